@@ -1,0 +1,94 @@
+// Parameter block of the fused task-mapped GEMM kernel (host + device).
+//
+// The kernel realises the spec's matmul_template with its
+// two fusion splice points: operand *loaders* are the prologue
+// splice (a direct/strided load, a cast, or the im2col gather of
+// conv2d_im2col_dag, proj/src/compute_ir.cpp:532-557), and the *epilogue op
+// list* plus the output *address map* are the epilogue splice (bijective
+// chains, fusion spec SPEC.md:379-387).  Everything here is plain data so it
+// can be built by the C++ planner and passed by value as a __grid_constant__.
+#pragma once
+#include <cstdint>
+
+#include "taskmap.cuh"
+
+namespace tmb {
+
+enum DType : int32_t { DT_F32 = 0, DT_BF16 = 1, DT_F16 = 2 };
+
+// Element address of GEMM coordinate (row, col, batch):
+//   (row / P) * s_hi + (row % P) * s_lo + col * s_col + batch * s_batch + offset
+// This is the canonical form every affine-bijective epilogue remap in the
+// reference's builders reduces to (row-major, transpose, NCHW re-index of the
+// im2col GEMM, reshape splits), cf. compute_ir.cpp:582-592.
+struct Addr {
+  int64_t P;  // >= 1
+  int64_t s_hi, s_lo, s_col, s_batch, offset;
+};
+
+enum EpiKind : int32_t {
+  EPI_ADD_C = 1, EPI_SUB_C, EPI_RSUB_C, EPI_MUL_C, EPI_DIV_C, EPI_RDIV_C, EPI_MAX_C, EPI_MIN_C,
+  EPI_ADD_T = 16, EPI_SUB_T, EPI_RSUB_T, EPI_MUL_T, EPI_DIV_T, EPI_RDIV_T, EPI_MAX_T, EPI_MIN_T,
+  EPI_RELU = 32, EPI_GELU_TANH, EPI_EXP, EPI_SQRT, EPI_NEG, EPI_ROUND_BF16
+};
+
+// One epilogue op; *_T kinds read a side tensor at `a` (dtype `dtype`).
+struct EpiOp {
+  int32_t kind;
+  int32_t dtype;
+  float c;
+  int32_t pad_;
+  const void* ptr;
+  Addr a;
+};
+
+constexpr int kMaxEpiOps = 8;
+
+enum LoaderKind : int32_t {
+  LD_TMA_K = 0,         // TMA tile load, K contiguous (K-major)
+  LD_TMA_MN = 1,        // TMA tile load, M/N contiguous (MN-major), B only, 16-bit
+  LD_GATHER = 2,        // predicated LSU gather of a strided operand (+ cast)
+  LD_IM2COL_GATHER = 3, // predicated im2col gather from any-strided X (A only)
+  LD_IM2COL_TMA = 4,    // TMA im2col mode on channels-last X (A only)
+  LD_FILTER_GATHER = 5  // conv filter W[F,C,Kh,Kw] with any strides (B only)
+};
+
+// A strided operand: element (row, k, batch) at
+//   (row / P) * s_hi + (row % P) * s_lo + k * s_k + batch * s_batch + offset
+struct Strided {
+  const void* ptr;
+  int32_t dtype;
+  int32_t pad_;
+  int64_t P, s_hi, s_lo, s_k, s_batch, offset;
+};
+
+// Convolution geometry (reference conv2d_im2col_dag arguments) plus element
+// strides of X[n,c,h,w] and W[f,c,kh,kw].  korder 0 = reference K order
+// r = c*Kh*Kw + fh*Kw + fw (compute_ir.cpp:540-542); korder 1 = (fh, fw, c),
+// the order TMA im2col produces (requires channels-last X and W).
+struct ConvGeom {
+  int32_t n, c, h, w, f, kh, kw, stride, pad, ho, wo, korder;
+  const void* x;
+  const void* wt;
+  int32_t x_dtype, w_dtype;
+  int64_t sx[4];
+  int64_t sw[4];
+};
+
+struct GemmParams {
+  int32_t M, N, K, batch;
+  int32_t num_kb;  // ceil(K / BK)
+  int32_t tiles_m, tiles_n;
+  int32_t a_loader, b_loader;
+  int32_t mn_lbo_sbo_swap;  // debug knob for the MN-major descriptor
+  Strided a, b;
+  ConvGeom conv;
+  tm::DevMapping tile_map;  // CTA -> (batch, tile_m, tile_n) task mapping
+  int32_t n_ops;
+  int32_t out_dtype;
+  EpiOp ops[kMaxEpiOps];
+  void* out;
+  Addr out_a;
+};
+
+}  // namespace tmb

@@ -1,0 +1,865 @@
+// Post-scheduling fusion for the B200 build (Hidet §4.2 / §5.2).
+//
+// partition()   groups the DAG around reduction anchors.
+// build_plan()  lowers each FusedSubgraph onto the task-mapped tcgen05 GEMM:
+//   * prologue  -> operand loader: direct/strided loads, pure re-index
+//                 prologues (the filter flatten Wf, transposes, Fig. 11's
+//                 A[99-i]) composed symbolically by substitution, and the
+//                 im2col gather recognised structurally (compute_ir.cpp:532-557);
+//   * epilogue  -> an op program run on the TMEM accumulator in registers plus
+//                 an output address map obtained by inverting each bijective
+//                 access (the "index remap" of fuse_epilogue).
+// bind_plan()   evaluates the symbolic address maps on the bound tensors'
+//               strides and fits them to the kernel's canonical Addr form.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <functional>
+#include <cstring>
+#include <random>
+#include <set>
+
+#include "json.hpp"
+#include "plan.hpp"
+
+namespace tmb {
+
+using namespace taskmap;
+
+// ============================================================ partition ==
+namespace {
+std::map<std::string, std::vector<std::string>> consumers_of(const ComputeDAG& dag) {
+  std::map<std::string, std::vector<std::string>> c;
+  for (const auto& n : dag.nodes) {
+    if (!n.is_computed()) continue;
+    std::vector<Expr> ls;
+    collect_loads(n.value, ls);
+    std::set<std::string> seen;
+    for (const auto& l : ls)
+      if (seen.insert(l->name).second) c[l->name].push_back(n.name);
+  }
+  return c;
+}
+
+bool is_output(const ComputeDAG& dag, const std::string& n) {
+  return std::find(dag.outputs.begin(), dag.outputs.end(), n) != dag.outputs.end();
+}
+
+// The single distinct access pattern with which `reader` loads `src` (nullptr
+// when it is read through two different index expressions).
+Expr unique_access(const TensorNode& reader, const std::string& src) {
+  std::vector<Expr> ls;
+  collect_loads(reader.value, ls);
+  Expr first;
+  for (const auto& l : ls) {
+    if (l->name != src) continue;
+    if (!first) first = l;
+    else if (!expr_equal(first, l)) return nullptr;
+  }
+  return first;
+}
+}  // namespace
+
+}  // namespace tmb
+
+std::vector<taskmap::FusedSubgraph> taskmap::partition(const taskmap::ComputeDAG& dag) {
+  using namespace tmb;
+  dag.validate();
+  auto cons = consumers_of(dag);
+  std::set<std::string> taken;
+  std::vector<FusedSubgraph> out;
+  auto single_use = [&](const std::string& n) { return cons[n].size() == 1 && !is_output(dag, n); };
+  for (const auto& r : dag.nodes) {
+    if (r.kind != NodeKind::GridReduce || taken.count(r.name)) continue;
+    FusedSubgraph sg;
+    sg.anchor = r.name;
+    taken.insert(r.name);
+    // prologues: injective, single-use producers of the anchor's operands
+    std::vector<Expr> ls;
+    collect_loads(r.value, ls);
+    std::set<std::string> seen;
+    for (const auto& l : ls) {
+      if (!seen.insert(l->name).second) continue;
+      const TensorNode& s = dag.at(l->name);
+      if (s.kind == NodeKind::GridCompute && !taken.count(s.name) && single_use(s.name) &&
+          classify(dag, s) != OpClass::Reduction) {
+        sg.prologue.push_back(s.name);
+        taken.insert(s.name);
+      }
+    }
+    // epilogue: chain of single-use consumers that read the chain bijectively
+    std::string cur = r.name;
+    for (;;) {
+      if (!single_use(cur)) break;
+      const TensorNode& e = dag.at(cons[cur][0]);
+      if (e.kind != NodeKind::GridCompute || taken.count(e.name)) break;
+      if (classify(dag, e) != OpClass::Bijective) break;
+      Expr acc = unique_access(e, cur);
+      if (!acc) break;
+      auto aff = analyze_affine_access(acc, e.axes);
+      if (!aff || !affine_access_bijective(*aff, e.axes, dag.at(cur).shape)) break;
+      sg.epilogue.push_back(e.name);
+      taken.insert(e.name);
+      cur = e.name;
+    }
+    sg.output = cur;
+    out.push_back(std::move(sg));
+  }
+  // anchor-free remainder: rule-based injective kernels
+  for (const auto& n : dag.nodes) {
+    if (n.kind != NodeKind::GridCompute || taken.count(n.name)) continue;
+    FusedSubgraph sg;
+    sg.epilogue.push_back(n.name);
+    sg.output = n.name;
+    out.push_back(std::move(sg));
+  }
+  return out;
+}
+
+namespace tmb {
+
+// ========================================================= IndexProgram ==
+IndexProgram IndexProgram::compile(const Expr& e, const std::vector<std::string>& slots) {
+  IndexProgram p;
+  std::function<void(const Expr&)> go = [&](const Expr& x) {
+    switch (x->kind) {
+      case ExprKind::IntImm: p.code.push_back({0, x->ival, BinOp::Add}); return;
+      case ExprKind::Var: {
+        auto it = std::find(slots.begin(), slots.end(), x->name);
+        if (it == slots.end()) fail("index expression uses unbound variable '", x->name, "'");
+        p.code.push_back({1, it - slots.begin(), BinOp::Add});
+        return;
+      }
+      case ExprKind::Binary:
+        go(x->args[0]);
+        go(x->args[1]);
+        p.code.push_back({2, 0, x->bop});
+        return;
+      case ExprKind::Unary:
+        if (x->uop == UnOp::Neg) { go(x->args[0]); p.code.push_back({3, 0, BinOp::Add}); return; }
+        if (x->uop == UnOp::CastI32) { go(x->args[0]); return; }
+        break;
+      case ExprKind::Select:
+        go(x->args[0]); go(x->args[1]); go(x->args[2]);
+        p.code.push_back({4, 0, BinOp::Add});
+        return;
+      default: break;
+    }
+    fail("unsupported construct in an index expression: ", expr_to_text(x));
+  };
+  go(e);
+  return p;
+}
+
+int64_t IndexProgram::eval(const int64_t* vars) const {
+  int64_t st[64];
+  int sp = 0;
+  for (const auto& in : code) {
+    switch (in.op) {
+      case 0: st[sp++] = in.v; break;
+      case 1: st[sp++] = vars[in.v]; break;
+      case 3: st[sp - 1] = -st[sp - 1]; break;
+      case 4: { const int64_t e = st[--sp], t = st[--sp], c = st[--sp]; st[sp++] = c ? t : e; break; }
+      default: {
+        const int64_t b = st[--sp], a = st[--sp];
+        int64_t r = 0;
+        switch (in.bop) {
+          case BinOp::Add: r = a + b; break;
+          case BinOp::Sub: r = a - b; break;
+          case BinOp::Mul: r = a * b; break;
+          case BinOp::Div: if (!b) fail("integer division by zero in index"); r = floordiv(a, b); break;
+          case BinOp::Mod: if (!b) fail("integer modulo by zero in index"); r = floormod(a, b); break;
+          case BinOp::Min: r = std::min(a, b); break;
+          case BinOp::Max: r = std::max(a, b); break;
+          case BinOp::And: r = a && b; break;
+          case BinOp::Or: r = a || b; break;
+          case BinOp::Lt: r = a < b; break;
+          case BinOp::Le: r = a <= b; break;
+          case BinOp::Gt: r = a > b; break;
+          case BinOp::Ge: r = a >= b; break;
+          case BinOp::Eq: r = a == b; break;
+          case BinOp::Ne: r = a != b; break;
+        }
+        st[sp++] = r;
+      }
+    }
+    if (sp >= 63) fail("index expression too deep");
+  }
+  return st[0];
+}
+
+// ============================================================ lowering ==
+namespace {
+const char* kRow = "__row";
+const char* kCol = "__col";
+const char* kBat = "__bat";
+
+bool contains_var(const Expr& e, const std::string& v) {
+  std::vector<std::string> vs;
+  collect_vars(e, vs);
+  return std::find(vs.begin(), vs.end(), v) != vs.end();
+}
+
+// Recognise the reference's im2col gather node (compute_ir.cpp:532-557) by
+// rebuilding candidates with our builder and comparing expressions.
+bool match_im2col(const ComputeDAG& dag, const TensorNode& col, ConvInfo& ci) {
+  if (col.axes.size() != 2) return false;
+  std::vector<Expr> ls;
+  collect_loads(col.value, ls);
+  if (ls.empty()) return false;
+  const std::string xname = ls[0]->name;
+  const TensorNode* x = dag.find(xname);
+  if (!x || x->kind != NodeKind::Input || x->shape.size() != 4) return false;
+  const int64_t n = x->shape[0], c = x->shape[1], h = x->shape[2], w = x->shape[3];
+  const int64_t gk = col.shape[0], gn = col.shape[1];
+  if (gk % c) return false;
+  const int64_t taps = gk / c;
+  for (int64_t kh = 1; kh <= taps; ++kh) {
+    if (taps % kh) continue;
+    const int64_t kw = taps / kh;
+    for (int64_t stride = 1; stride <= 8; ++stride)
+      for (int64_t pad = 0; pad <= std::max(kh, kw); ++pad) {
+        if (kh > h + 2 * pad || kw > w + 2 * pad) continue;
+        const int64_t ho = conv_out_extent(h, kh, stride, pad), wo = conv_out_extent(w, kw, stride, pad);
+        if (ho <= 0 || wo <= 0 || n * ho * wo != gn) continue;
+        ComputeDAG ref = conv2d_im2col_dag(n, c, h, w, 1, kh, kw, stride, pad, x->dtype);
+        const TensorNode& rc = ref.at("Col");
+        Expr cand = substitute(rc.value, {{"r", var(col.axes[0].name)}, {"s", var(col.axes[1].name)}});
+        cand = rewrite_loads(cand, [&](const ExprNode& l) -> std::optional<Expr> {
+          return load(xname, l.args);
+        });
+        if (expr_equal(cand, col.value)) {
+          ci = ConvInfo{n, c, h, w, 0, kh, kw, stride, pad, ho, wo, xname, ""};
+          return true;
+        }
+      }
+  }
+  return false;
+}
+
+// The filter flatten Wf[p, r] = W[p, r/(kh kw), (r/kw)%kh, r%kw] (compute_ir.cpp:558-569).
+bool match_filter(const ComputeDAG& dag, const TensorNode& wf, const ConvInfo& ci, std::string& wname) {
+  if (wf.value->kind != ExprKind::Load || wf.axes.size() != 2) return false;
+  const TensorNode* w = dag.find(wf.value->name);
+  if (!w || w->kind != NodeKind::Input || w->shape.size() != 4) return false;
+  ComputeDAG ref = conv2d_im2col_dag(ci.n, ci.c, ci.h, ci.w, w->shape[0], ci.kh, ci.kw, ci.stride, ci.pad, w->dtype);
+  Expr cand = substitute(ref.at("Wf").value, {{"p", var(wf.axes[0].name)}, {"r", var(wf.axes[1].name)}});
+  cand = rewrite_loads(cand, [&](const ExprNode& l) -> std::optional<Expr> { return load(w->name, l.args); });
+  if (!expr_equal(cand, wf.value)) return false;
+  wname = w->name;
+  return true;
+}
+
+// Inverse of an affine bijective access: expressions for the reader's axes in
+// terms of the source coordinates `src` (already in slot variables).
+std::map<std::string, Expr> invert_access(const TensorNode& reader, const std::vector<AffineIndex>& acc,
+                                          const std::vector<Expr>& src) {
+  std::map<std::string, Expr> m;
+  for (const auto& a : reader.axes) m[a.name] = imm(0);  // unit axes
+  for (size_t d = 0; d < acc.size(); ++d) {
+    int64_t lo = acc[d].offset;
+    for (const auto& t : acc[d].terms)
+      if (t.coeff < 0) lo += t.coeff * (reader.axes[t.axis].extent - 1);
+    Expr v = fold(sub(src[d], imm(lo)));
+    for (const auto& t : acc[d].terms) {
+      const int64_t e = reader.axes[t.axis].extent, c = std::llabs(t.coeff);
+      Expr x = fold(mod(fold(div(v, imm(c))), imm(e)));
+      if (t.coeff < 0) x = fold(sub(imm(e - 1), x));
+      m[reader.axes[t.axis].name] = x;
+    }
+  }
+  return m;
+}
+
+struct EpiBuilder {
+  const ComputeDAG& dag;
+  SubgraphPlan& sp;
+  std::map<std::string, Expr> coords;  // current level axes -> slot exprs
+  const std::string* pred = nullptr;   // tensor holding the accumulator value
+
+  bool has_acc(const Expr& e) {
+    if (e->kind == ExprKind::Load && e->name == *pred) return true;
+    return std::any_of(e->args.begin(), e->args.end(), [&](const Expr& a) { return has_acc(a); });
+  }
+
+  // wildcard match against gelu_tanh(__x__)
+  bool match_gelu(const Expr& e, Expr& x) {
+    static const Expr tmpl = gelu_tanh(var("__gelu_x__"));
+    Expr bound;
+    std::function<bool(const Expr&, const Expr&)> m = [&](const Expr& t, const Expr& s) -> bool {
+      if (t->kind == ExprKind::Var && t->name == "__gelu_x__") {
+        if (!bound) { bound = s; return true; }
+        return expr_equal(bound, s);
+      }
+      if (t->kind != s->kind || t->args.size() != s->args.size()) return false;
+      if (t->kind == ExprKind::FloatImm && t->fval != s->fval) return false;
+      if (t->kind == ExprKind::IntImm && t->ival != s->ival) return false;
+      if (t->kind == ExprKind::Binary && t->bop != s->bop) return false;
+      if (t->kind == ExprKind::Unary && t->uop != s->uop) return false;
+      if (t->kind == ExprKind::Var || t->kind == ExprKind::Load) return false;
+      for (size_t i = 0; i < t->args.size(); ++i)
+        if (!m(t->args[i], s->args[i])) return false;
+      return true;
+    };
+    if (!m(tmpl, e)) return false;
+    x = bound;
+    return true;
+  }
+
+  int side_of(const Expr& ld) {
+    const TensorNode* t = dag.find(ld->name);
+    if (!t) fail("epilogue reads unknown tensor '", ld->name, "'");
+    AddrExpr a;
+    a.tensor = ld->name;
+    for (const auto& ix : ld->args) a.idx.push_back(fold(substitute(ix, coords)));
+    sp.sides.push_back(std::move(a));
+    return static_cast<int>(sp.sides.size()) - 1;
+  }
+
+  void walk(const Expr& e) {
+    if (e->kind == ExprKind::Load && e->name == *pred) return;  // the accumulator
+    Expr gx;
+    if (match_gelu(e, gx) && has_acc(gx)) {
+      walk(gx);
+      sp.ops.push_back({EPI_GELU_TANH});
+      return;
+    }
+    if (e->kind == ExprKind::Unary) {
+      walk(e->args[0]);
+      switch (e->uop) {
+        case UnOp::Relu: sp.ops.push_back({EPI_RELU}); return;
+        case UnOp::Neg: sp.ops.push_back({EPI_NEG}); return;
+        case UnOp::Exp: sp.ops.push_back({EPI_EXP}); return;
+        case UnOp::Sqrt: sp.ops.push_back({EPI_SQRT}); return;
+        case UnOp::CastF32: return;
+        default: fail("epilogue op ", unop_name(e->uop), " is not supported on the device");
+      }
+    }
+    if (e->kind == ExprKind::Binary) {
+      const bool l = has_acc(e->args[0]), r = has_acc(e->args[1]);
+      if (l == r) fail("epilogue expression is not a single-use chain of the accumulator: ", expr_to_text(e));
+      const Expr& spine = l ? e->args[0] : e->args[1];
+      const Expr side = fold(l ? e->args[1] : e->args[0]);
+      walk(spine);
+      EpiStep st{0};
+      const bool is_const = side->kind == ExprKind::FloatImm || side->kind == ExprKind::IntImm;
+      if (is_const) st.c = static_cast<float>(side->kind == ExprKind::FloatImm ? side->fval : static_cast<double>(side->ival));
+      else if (side->kind == ExprKind::Load) st.side = side_of(side);
+      else fail("epilogue side operand must be a constant or a tensor element: ", expr_to_text(side));
+      const int t = is_const ? 0 : (EPI_ADD_T - EPI_ADD_C);
+      switch (e->bop) {
+        case BinOp::Add: st.kind = EPI_ADD_C + t; break;
+        case BinOp::Sub: st.kind = (l ? EPI_SUB_C : EPI_RSUB_C) + t; break;
+        case BinOp::Mul: st.kind = EPI_MUL_C + t; break;
+        case BinOp::Div: st.kind = (l ? EPI_DIV_C : EPI_RDIV_C) + t; break;
+        case BinOp::Max: st.kind = EPI_MAX_C + t; break;
+        case BinOp::Min: st.kind = EPI_MIN_C + t; break;
+        default: fail("epilogue operator ", binop_name(e->bop), " is not supported on the device");
+      }
+      sp.ops.push_back(st);
+      return;
+    }
+    fail("unsupported epilogue expression: ", expr_to_text(e));
+  }
+};
+
+SubgraphPlan lower_subgraph(const ComputeDAG& dag, const FusedSubgraph& sg) {
+  SubgraphPlan sp;
+  sp.sg = sg;
+  if (sg.anchor.empty())
+    fail("subgraph '", sg.output, "' has no reduction anchor; rule-based injective kernels are out of scope");
+  const TensorNode& r = dag.at(sg.anchor);
+  if (r.combiner != Combiner::Sum) fail("anchor '", r.name, "': only sum reductions lower to tcgen05");
+  if (r.reduce_axes.size() != 1) fail("anchor '", r.name, "': exactly one reduce axis is supported");
+  if (r.axes.size() != 2 && r.axes.size() != 3) fail("anchor '", r.name, "': 2 or 3 spatial axes expected");
+  Expr v = r.value;
+  if (v->kind != ExprKind::Binary || v->bop != BinOp::Mul || v->args[0]->kind != ExprKind::Load ||
+      v->args[1]->kind != ExprKind::Load)
+    fail("anchor '", r.name, "': value must be the product of two tensor elements");
+  const std::string kname = r.reduce_axes[0].name;
+  Expr L[2] = {v->args[0], v->args[1]};
+  auto uses = [&](const Expr& l, const std::string& ax) {
+    return std::any_of(l->args.begin(), l->args.end(), [&](const Expr& i) { return contains_var(i, ax); });
+  };
+  std::string own[2], batch;
+  for (const auto& ax : r.axes) {
+    const bool u0 = uses(L[0], ax.name), u1 = uses(L[1], ax.name);
+    if (u0 && u1) {
+      if (!batch.empty()) fail("anchor '", r.name, "': at most one batch axis");
+      batch = ax.name;
+    } else if (u0 || u1) {
+      std::string& slot = own[u0 ? 0 : 1];
+      if (!slot.empty()) fail("anchor '", r.name, "': operand owns two spatial axes");
+      slot = ax.name;
+    } else {
+      fail("anchor '", r.name, "': axis '", ax.name, "' unused by the operands");
+    }
+  }
+  if (own[0].empty() || own[1].empty()) fail("anchor '", r.name, "': not a matrix product");
+  if (!uses(L[0], kname) || !uses(L[1], kname)) fail("anchor '", r.name, "': reduce axis missing from an operand");
+
+  const bool pro0 = std::find(sg.prologue.begin(), sg.prologue.end(), L[0]->name) != sg.prologue.end();
+  const bool pro1 = std::find(sg.prologue.begin(), sg.prologue.end(), L[1]->name) != sg.prologue.end();
+  ConvInfo ci{};
+  int im2col_side = -1;
+  if (pro0 && match_im2col(dag, dag.at(L[0]->name), ci)) im2col_side = 0;
+  else if (pro1 && match_im2col(dag, dag.at(L[1]->name), ci)) im2col_side = 1;
+  // orientation: im2col operand provides the rows (pixels on TMEM lanes);
+  // otherwise the operand owning the first non-batch anchor axis
+  int ia = 0;
+  if (im2col_side >= 0) ia = im2col_side;
+  else {
+    for (const auto& ax : r.axes)
+      if (ax.name == own[0] || ax.name == own[1]) { ia = ax.name == own[0] ? 0 : 1; break; }
+  }
+  const int ib = 1 - ia;
+  auto extent = [&](const std::string& n) {
+    for (const auto& ax : r.axes) if (ax.name == n) return ax.extent;
+    return int64_t(1);
+  };
+  sp.M = extent(own[ia]);
+  sp.N = extent(own[ib]);
+  sp.K = r.reduce_axes[0].extent;
+  sp.batch = batch.empty() ? 1 : extent(batch);
+
+  // operand address maps: rename anchor axes to slot vars
+  auto lower_operand = [&](int which, OperandPlan& op) {
+    const Expr& ld = L[which];
+    std::map<std::string, Expr> ren = {{own[which], var(kRow)}, {kname, var(kCol)}};
+    if (!batch.empty()) ren[batch] = var(kBat);
+    std::vector<Expr> idx;
+    for (const auto& i : ld->args) idx.push_back(substitute(i, ren));
+    const TensorNode& s = dag.at(ld->name);
+    const bool is_pro = (which == 0 ? pro0 : pro1);
+    if (which == im2col_side) {
+      // the anchor must read Col[k, pixel] directly
+      if (idx.size() != 2 || !expr_equal(idx[0], var(kCol)) || !expr_equal(idx[1], var(kRow)))
+        fail("anchor reads the im2col node through a non-identity index");
+      op.kind = OperandPlan::Im2col;
+      op.conv = ci;
+      return;
+    }
+    if (!is_pro) {
+      // a graph input, or a tensor materialised by an earlier fused kernel
+      op.kind = OperandPlan::Strided;
+      op.addr.tensor = s.name;
+      op.addr.idx = idx;
+      return;
+    }
+    // prologue node
+    if (im2col_side >= 0) {
+      std::string wname;
+      if (match_filter(dag, s, ci, wname) && idx.size() == 2 && expr_equal(idx[0], var(kRow)) &&
+          expr_equal(idx[1], var(kCol))) {
+        op.kind = OperandPlan::ConvFilter;
+        op.conv = ci;
+        op.conv.w_tensor = wname;
+        op.conv.f = dag.at(wname).shape[0];
+        return;
+      }
+    }
+    if (s.value->kind != ExprKind::Load || dag.at(s.value->name).kind != NodeKind::Input)
+      fail("prologue '", s.name, "' is not a pure re-index of a graph input (arithmetic prologues are out of scope)");
+    std::map<std::string, Expr> sub_map;
+    for (size_t d = 0; d < s.axes.size(); ++d) sub_map[s.axes[d].name] = idx[d];
+    op.kind = OperandPlan::Strided;
+    op.addr.tensor = s.value->name;
+    for (const auto& i : s.value->args) op.addr.idx.push_back(fold(substitute(i, sub_map)));
+  };
+  lower_operand(ia, sp.a);
+  lower_operand(ib, sp.b);
+  if (sp.a.kind == OperandPlan::Im2col && sp.b.kind == OperandPlan::Strided) {
+    // keep as strided filter (e.g. an already-flattened weight input)
+  }
+
+  // epilogue chain: accumulate coordinate maps level by level
+  EpiBuilder eb{dag, sp, {}, nullptr};
+  {
+    std::map<std::string, Expr> m = {{own[ia], var(kRow)}, {own[ib], var(kCol)}};
+    if (!batch.empty()) m[batch] = var(kBat);
+    eb.coords = m;
+  }
+  std::string pred = r.name;
+  std::vector<Expr> pred_coords;  // predecessor coords in slot vars (in its axis order)
+  for (const auto& ax : r.axes) pred_coords.push_back(eb.coords.at(ax.name));
+  for (const auto& en : sg.epilogue) {
+    const TensorNode& e = dag.at(en);
+    Expr acc = unique_access(e, pred);
+    auto aff = analyze_affine_access(acc, e.axes);
+    std::map<std::string, Expr> inv = invert_access(e, *aff, pred_coords);
+    eb.coords = inv;
+    eb.pred = &pred;
+    eb.walk(e.value);
+    pred = en;
+    pred_coords.clear();
+    for (const auto& ax : e.axes) pred_coords.push_back(eb.coords.at(ax.name));
+  }
+  sp.out.tensor = sg.output;
+  sp.out.idx = pred_coords;
+  return sp;
+}
+}  // namespace
+
+std::string SubgraphPlan::describe() const {
+  std::ostringstream o;
+  auto idxs = [](const AddrExpr& a) {
+    std::string s = a.tensor + "[";
+    for (size_t i = 0; i < a.idx.size(); ++i) s += (i ? ", " : "") + expr_to_text(a.idx[i]);
+    return s + "]";
+  };
+  auto opd = [&](const OperandPlan& p) {
+    if (p.kind == OperandPlan::Im2col) return std::string("im2col(") + p.conv.x_tensor + ")";
+    if (p.kind == OperandPlan::ConvFilter) return std::string("filter(") + p.conv.w_tensor + ")";
+    return idxs(p.addr);
+  };
+  o << "{\"anchor\":" << tmjson::quote(sg.anchor) << ",\"M\":" << M << ",\"N\":" << N << ",\"K\":" << K
+    << ",\"batch\":" << batch << ",\"A\":" << tmjson::quote(opd(a)) << ",\"B\":" << tmjson::quote(opd(b))
+    << ",\"prologue\":[";
+  for (size_t i = 0; i < sg.prologue.size(); ++i) o << (i ? "," : "") << tmjson::quote(sg.prologue[i]);
+  o << "],\"epilogue\":[";
+  for (size_t i = 0; i < sg.epilogue.size(); ++i) o << (i ? "," : "") << tmjson::quote(sg.epilogue[i]);
+  o << "],\"ops\":[";
+  for (size_t i = 0; i < ops.size(); ++i) {
+    o << (i ? "," : "") << "{\"kind\":" << ops[i].kind << ",\"c\":" << ops[i].c;
+    if (ops[i].side >= 0) o << ",\"side\":" << tmjson::quote(idxs(sides[ops[i].side]));
+    o << "}";
+  }
+  o << "],\"out\":" << tmjson::quote(idxs(out)) << "}";
+  return o.str();
+}
+
+std::unique_ptr<Plan> build_plan(const ComputeDAG& dag, const ScheduleConfig& cfg, int device) {
+  auto plan = std::make_unique<Plan>();
+  plan->dag = dag;
+  plan->cfg = cfg;
+  plan->device = device;
+  std::set<std::string> produced;
+  for (const auto& sg : partition(dag)) {
+    plan->kernels.push_back(lower_subgraph(dag, sg));
+    produced.insert(sg.output);
+  }
+  for (const auto& o : dag.outputs)
+    if (!produced.count(o)) fail("output '", o, "' is not produced by a fused kernel");
+  for (const auto& s : produced)
+    if (!is_output(dag, s)) plan->intermediates.push_back(s);
+  return plan;
+}
+
+// ================================================================ binding ==
+namespace {
+struct Bound {
+  tm_tensor t;
+};
+
+// Fitted canonical form of addr(x0, x1, x2) = sum_d stride_d * idx_d.
+struct Fit {
+  int64_t P, hi, lo, c1, c2, off;
+};
+
+bool fit_address(const AddrExpr& a, const tm_tensor& t, int64_t n0, int64_t n1, int64_t n2, Fit& f,
+                 std::string& why) {
+  if (static_cast<int>(a.idx.size()) != t.rank) { why = "rank mismatch"; return false; }
+  std::vector<IndexProgram> progs;
+  for (const auto& e : a.idx) progs.push_back(IndexProgram::compile(e, {kRow, kCol, kBat}));
+  auto addr = [&](int64_t x0, int64_t x1, int64_t x2, bool& oob) {
+    const int64_t v[3] = {x0, x1, x2};
+    int64_t s = 0;
+    for (int d = 0; d < t.rank; ++d) {
+      const int64_t i = progs[d].eval(v);
+      if (i < 0 || i >= t.shape[d]) oob = true;
+      s += i * t.stride[d];
+    }
+    return s;
+  };
+  bool oob = false;
+  f.off = addr(0, 0, 0, oob);
+  f.c1 = n1 > 1 ? addr(0, 1, 0, oob) - f.off : 0;
+  f.c2 = n2 > 1 ? addr(0, 0, 1, oob) - f.off : 0;
+  for (int64_t x = 0; x < n1; ++x)
+    if (addr(0, x, 0, oob) != f.off + x * f.c1) { why = "not affine along the column/K axis"; return false; }
+  for (int64_t x = 0; x < n2; ++x)
+    if (addr(0, 0, x, oob) != f.off + x * f.c2) { why = "not affine along the batch axis"; return false; }
+  f.lo = n0 > 1 ? addr(1, 0, 0, oob) - f.off : 0;
+  f.P = std::max<int64_t>(n0, 1);
+  f.hi = 0;
+  for (int64_t x = 1; x < n0; ++x)
+    if (addr(x, 0, 0, oob) - f.off != x * f.lo) { f.P = x; f.hi = addr(x, 0, 0, oob) - f.off; break; }
+  for (int64_t x = 0; x < n0; ++x)
+    if (addr(x, 0, 0, oob) - f.off != (x / f.P) * f.hi + (x % f.P) * f.lo) {
+      why = "row map is not of the form (r/P)*a + (r%P)*b";
+      return false;
+    }
+  std::mt19937_64 rng(1234);
+  for (int s = 0; s < 512; ++s) {
+    const int64_t x0 = s < 8 ? ((s & 1) ? n0 - 1 : 0) : static_cast<int64_t>(rng() % n0);
+    const int64_t x1 = s < 8 ? ((s & 2) ? n1 - 1 : 0) : static_cast<int64_t>(rng() % n1);
+    const int64_t x2 = s < 8 ? ((s & 4) ? n2 - 1 : 0) : static_cast<int64_t>(rng() % n2);
+    if (addr(x0, x1, x2, oob) != f.off + (x0 / f.P) * f.hi + (x0 % f.P) * f.lo + x1 * f.c1 + x2 * f.c2) {
+      why = "address map is not separable";
+      return false;
+    }
+  }
+  if (oob) { why = "index out of bounds"; return false; }
+  return true;
+}
+
+int esize(int dt) { return dt == TM_F32 ? 4 : 2; }
+
+Addr to_addr(const Fit& f) { return Addr{f.P, f.hi, f.lo, f.c1, f.c2, f.off}; }
+
+const tm_tensor& lookup(const std::map<std::string, tm_tensor>& env, const std::string& n) {
+  auto it = env.find(n);
+  if (it == env.end()) fail("tensor '", n, "' is not bound");
+  return it->second;
+}
+
+// CTA -> tile task mapping over the (batch, tiles_m, tiles_n) domain:
+// raster 0: repeat(r) * spatial(g)  (each wave sweeps a g-block of tiles)
+// raster 1: spatial(g) * repeat(r)  (each CTA owns a contiguous r-block)
+tm::DevMapping tile_mapping(int64_t B, int64_t TM, int64_t TN, int grid, int raster, int& used) {
+  const int64_t dom[3] = {B, TM, TN};
+  int64_t best_cost = INT64_MAX, bg[3] = {1, 1, 1};
+  for (int64_t gb = 1; gb <= std::min<int64_t>(B, grid); ++gb)
+    for (int64_t gm = 1; gm <= std::min<int64_t>(TM, grid / gb); ++gm) {
+      const int64_t gn = std::min<int64_t>(TN, grid / (gb * gm));
+      if (gn < 1) continue;
+      const int64_t g[3] = {gb, gm, gn};
+      int64_t waves = 1;
+      for (int d = 0; d < 3; ++d) waves *= (dom[d] + g[d] - 1) / g[d];
+      // primary: fewest tile rounds; secondary: more CTAs (less per-CTA work)
+      const int64_t cost = waves * 4096 - gb * gm * gn;
+      if (cost < best_cost) { best_cost = cost; bg[0] = gb; bg[1] = gm; bg[2] = gn; }
+    }
+  tm::DevMapping m{};
+  m.rank = 3;
+  m.n_atoms = 2;
+  const int rep = raster == 0 ? 0 : 1, spa = 1 - rep;
+  m.is_spatial[rep] = 0;
+  m.is_spatial[spa] = 1;
+  m.workers = 1;
+  m.tasks = 1;
+  for (int d = 0; d < 3; ++d) {
+    const int64_t r = (dom[d] + bg[d] - 1) / bg[d];
+    m.dims[rep][d] = static_cast<int32_t>(r);
+    m.dims[spa][d] = static_cast<int32_t>(bg[d]);
+    m.tasks *= static_cast<uint32_t>(r);
+    m.workers *= static_cast<uint32_t>(bg[d]);
+    m.shape[d] = static_cast<int32_t>(r * bg[d]);
+  }
+  used = static_cast<int>(m.workers);
+  return m;
+}
+
+bool tma_ok_kmajor(const Fit& f, const tm_tensor& t, int64_t rows, int want_dt) {
+  const int es = esize(t.dtype);
+  if (t.dtype != want_dt) return false;
+  if (f.c1 != 1 || f.P < rows) return false;
+  if ((f.lo * es) % 16 || (f.c2 * es) % 16 || f.lo <= 0) return false;
+  const uintptr_t base = reinterpret_cast<uintptr_t>(t.data) + f.off * es;
+  return base % 16 == 0;
+}
+
+bool tma_ok_mnmajor(const Fit& f, const tm_tensor& t, int64_t rows) {
+  if (t.dtype != TM_BF16 && t.dtype != TM_F16) return false;
+  const int es = esize(t.dtype);
+  if (f.lo != 1 || f.P < rows || f.c1 <= 0) return false;
+  if ((f.c1 * es) % 16 || (f.c2 * es) % 16) return false;
+  return (reinterpret_cast<uintptr_t>(t.data) + f.off * es) % 16 == 0;
+}
+}  // namespace
+
+Exec::~Exec() {
+  for (void* p : scratch) cudaFree(p);
+}
+
+std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n_in,
+                                const tm_tensor* outputs, int n_out) {
+  const ComputeDAG& dag = plan.dag;
+  if (n_in != static_cast<int>(dag.inputs.size()))
+    fail("expected ", dag.inputs.size(), " input tensors, got ", n_in);
+  if (n_out != static_cast<int>(dag.outputs.size()))
+    fail("expected ", dag.outputs.size(), " output tensors, got ", n_out);
+  std::map<std::string, tm_tensor> env;
+  auto check = [&](const std::string& name, const tm_tensor& t) {
+    const TensorNode& n = dag.at(name);
+    if (t.rank != static_cast<int>(n.shape.size())) fail("tensor '", name, "' has wrong rank");
+    for (int d = 0; d < t.rank; ++d)
+      if (t.shape[d] != n.shape[d]) fail("tensor '", name, "' has wrong shape at dim ", d);
+    if (t.dtype != TM_F32 && t.dtype != TM_BF16 && t.dtype != TM_F16) fail("tensor '", name, "' has unsupported dtype");
+    if (!t.data) fail("tensor '", name, "' has a null data pointer");
+    env[name] = t;
+  };
+  for (int i = 0; i < n_in; ++i) check(dag.inputs[i], inputs[i]);
+  for (int i = 0; i < n_out; ++i) check(dag.outputs[i], outputs[i]);
+  auto ex = std::make_unique<Exec>();
+  int idt = TM_BF16;
+  for (int i = 0; i < n_in; ++i)
+    if (inputs[i].dtype == TM_F32) idt = TM_F32;
+  for (const auto& name : plan.intermediates) {
+    const TensorNode& n = dag.at(name);
+    tm_tensor t{};
+    t.dtype = idt;
+    t.rank = static_cast<int>(n.shape.size());
+    int64_t numel = 1;
+    for (int d = t.rank - 1; d >= 0; --d) {
+      t.shape[d] = n.shape[d];
+      t.stride[d] = numel;
+      numel *= n.shape[d];
+    }
+    void* p = nullptr;
+    if (cudaMalloc(&p, numel * esize(idt)) != cudaSuccess) fail("cudaMalloc failed for intermediate '", name, "'");
+    ex->scratch.push_back(p);
+    t.data = p;
+    env[name] = t;
+  }
+  const int sms = num_sms(plan.device);
+  for (const auto& sp : plan.kernels) {
+    BoundKernel k{};
+    GemmParams& p = k.p;
+    p.M = static_cast<int32_t>(sp.M);
+    p.N = static_cast<int32_t>(sp.N);
+    p.K = static_cast<int32_t>(sp.K);
+    p.batch = static_cast<int32_t>(sp.batch);
+    // math kind
+    std::string math = plan.cfg.math;
+    const tm_tensor* opa = sp.a.kind == OperandPlan::Strided ? &lookup(env, sp.a.addr.tensor) : &lookup(env, sp.a.conv.x_tensor);
+    const tm_tensor* opb = sp.b.kind == OperandPlan::Strided ? &lookup(env, sp.b.addr.tensor) : &lookup(env, sp.b.conv.w_tensor);
+    if (math == "auto") math = (opa->dtype == TM_F32 || opb->dtype == TM_F32) ? "tf32" : "bf16";
+    if (math == "fp32_simt") k.simt = 1;
+    k.tf32 = math == "tf32";
+    const int BK = k.tf32 ? 32 : 64;
+    const int want_dt = k.tf32 ? TM_F32 : TM_BF16;
+    k.bn = plan.cfg.block_n;
+    if (k.bn < 16 || k.bn > 256 || k.bn % 16) fail("block_n must be 16..256 in steps of 16");
+    k.stages = plan.cfg.pipeline ? plan.cfg.stages : 2;
+    p.num_kb = static_cast<int32_t>((sp.K + BK - 1) / BK);
+    p.tiles_m = static_cast<int32_t>((sp.M + 127) / 128);
+    p.tiles_n = static_cast<int32_t>((sp.N + k.bn - 1) / k.bn);
+    // ---- operand A
+    auto strided_of = [&](const Fit& f, const tm_tensor& t) {
+      Strided s{};
+      s.ptr = t.data;
+      s.dtype = t.dtype;
+      s.P = f.P; s.s_hi = f.hi; s.s_lo = f.lo; s.s_k = f.c1; s.s_batch = f.c2; s.offset = f.off;
+      return s;
+    };
+    std::string why;
+    bool im2col_tma = false;
+    if (sp.a.kind == OperandPlan::Im2col) {
+      const ConvInfo& c = sp.a.conv;
+      const tm_tensor& x = *opa;
+      ConvGeom& g = p.conv;
+      g.n = c.n; g.c = c.c; g.h = c.h; g.w = c.w; g.kh = c.kh; g.kw = c.kw; g.stride = c.stride;
+      g.pad = c.pad; g.ho = c.ho; g.wo = c.wo; g.x = x.data; g.x_dtype = x.dtype;
+      for (int d = 0; d < 4; ++d) g.sx[d] = x.stride[d];
+      const bool cl = x.stride[1] == 1 && x.stride[3] == c.c && x.stride[2] == c.w * c.c && x.stride[0] == c.h * c.w * c.c;
+      im2col_tma = !k.tf32 && x.dtype == TM_BF16 && cl && c.c % BK == 0 && c.stride <= 8 &&
+                   c.pad <= 127 && (c.kh - 1 - c.pad) <= 128 && c.kh <= 127 && c.kw <= 127 &&
+                   (reinterpret_cast<uintptr_t>(x.data) % 16 == 0) &&
+                   sp.b.kind == OperandPlan::ConvFilter && plan.cfg.split_k >= 1;
+      g.korder = im2col_tma ? 1 : 0;
+      p.a_loader = im2col_tma ? LD_IM2COL_TMA : LD_IM2COL_GATHER;
+      if (im2col_tma) {
+        const uint64_t dims[4] = {(uint64_t)c.c, (uint64_t)c.w, (uint64_t)c.h, (uint64_t)c.n};
+        const uint64_t strides[3] = {(uint64_t)x.stride[3] * 2, (uint64_t)x.stride[2] * 2, (uint64_t)x.stride[0] * 2};
+        make_tma_im2col(k.tma_a, x.data, x.dtype, dims, strides, static_cast<int>(c.pad),
+                        static_cast<int>(c.pad - (c.kh - 1)), static_cast<int>(c.stride), BK, 128);
+      }
+    } else {
+      Fit f;
+      if (!fit_address(sp.a.addr, *opa, sp.M, sp.K, sp.batch, f, why)) fail("operand A '", sp.a.addr.tensor, "': ", why);
+      p.a = strided_of(f, *opa);
+      if (tma_ok_kmajor(f, *opa, sp.M, want_dt)) {
+        p.a_loader = LD_TMA_K;
+        const uint64_t dims[3] = {(uint64_t)sp.K, (uint64_t)sp.M, (uint64_t)sp.batch};
+        const uint64_t strides[2] = {(uint64_t)(f.lo * esize(opa->dtype)),
+                                     (uint64_t)(std::max<int64_t>(f.c2, f.lo * sp.M) * esize(opa->dtype))};
+        const uint32_t box[3] = {(uint32_t)BK, 128u, 1u};
+        make_tma_2d3d(k.tma_a, static_cast<const char*>(opa->data) + f.off * esize(opa->dtype), opa->dtype, 3, dims, strides, box);
+      } else {
+        p.a_loader = LD_GATHER;
+      }
+    }
+    // ---- operand B
+    if (sp.b.kind == OperandPlan::ConvFilter) {
+      const tm_tensor& w = *opb;
+      ConvGeom& g = p.conv;
+      g.f = static_cast<int32_t>(sp.N);
+      g.wt = w.data;
+      g.w_dtype = w.dtype;
+      for (int d = 0; d < 4; ++d) g.sw[d] = w.stride[d];
+      const ConvInfo& c = sp.b.conv;
+      // K-major filter view: korder 0 needs OIHW-contiguous, korder 1 needs OHWI
+      const bool oihw = w.stride[3] == 1 && w.stride[2] == c.kw && w.stride[1] == c.kh * c.kw;
+      const bool ohwi = w.stride[1] == 1 && w.stride[3] == c.c && w.stride[2] == c.kw * c.c;
+      const bool lin = g.korder == 0 ? oihw : ohwi;
+      const int64_t row_stride = w.stride[0];
+      if (lin && w.dtype == want_dt && (row_stride * esize(w.dtype)) % 16 == 0 &&
+          reinterpret_cast<uintptr_t>(w.data) % 16 == 0) {
+        p.b_loader = LD_TMA_K;
+        const uint64_t dims[3] = {(uint64_t)sp.K, (uint64_t)sp.N, 1};
+        const uint64_t strides[2] = {(uint64_t)(row_stride * esize(w.dtype)), (uint64_t)(row_stride * sp.N * esize(w.dtype))};
+        const uint32_t box[3] = {(uint32_t)BK, (uint32_t)k.bn, 1u};
+        make_tma_2d3d(k.tma_b, w.data, w.dtype, 3, dims, strides, box);
+      } else {
+        p.b_loader = LD_FILTER_GATHER;
+      }
+    } else {
+      if (sp.b.kind != OperandPlan::Strided) fail("operand B must be a strided tensor or a conv filter");
+      Fit f;
+      if (!fit_address(sp.b.addr, *opb, sp.N, sp.K, sp.batch, f, why)) fail("operand B '", sp.b.addr.tensor, "': ", why);
+      p.b = strided_of(f, *opb);
+      if (tma_ok_kmajor(f, *opb, sp.N, want_dt)) {
+        p.b_loader = LD_TMA_K;
+        const uint64_t dims[3] = {(uint64_t)sp.K, (uint64_t)sp.N, (uint64_t)sp.batch};
+        const uint64_t strides[2] = {(uint64_t)(f.lo * esize(opb->dtype)),
+                                     (uint64_t)(std::max<int64_t>(f.c2, f.lo * sp.N) * esize(opb->dtype))};
+        const uint32_t box[3] = {(uint32_t)BK, (uint32_t)k.bn, 1u};
+        make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * esize(opb->dtype), opb->dtype, 3, dims, strides, box);
+      } else if (!k.tf32 && k.bn % 64 == 0 && tma_ok_mnmajor(f, *opb, sp.N)) {
+        p.b_loader = LD_TMA_MN;
+        const uint64_t dims[3] = {(uint64_t)sp.N, (uint64_t)sp.K, (uint64_t)sp.batch};
+        const uint64_t strides[2] = {(uint64_t)(f.c1 * 2), (uint64_t)(std::max<int64_t>(f.c2, f.c1 * sp.K) * 2)};
+        const uint32_t box[3] = {64u, (uint32_t)BK, 1u};
+        make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * 2, opb->dtype, 3, dims, strides, box);
+      } else {
+        p.b_loader = LD_GATHER;
+      }
+    }
+    // ---- epilogue
+    if (sp.ops.size() > static_cast<size_t>(kMaxEpiOps)) fail("epilogue longer than ", kMaxEpiOps, " ops");
+    p.n_ops = static_cast<int32_t>(sp.ops.size());
+    for (size_t i = 0; i < sp.ops.size(); ++i) {
+      EpiOp& o = p.ops[i];
+      o.kind = sp.ops[i].kind;
+      o.c = sp.ops[i].c;
+      o.a = Addr{1, 0, 0, 0, 0, 0};
+      if (sp.ops[i].side >= 0) {
+        const AddrExpr& ae = sp.sides[sp.ops[i].side];
+        const tm_tensor& t = lookup(env, ae.tensor);
+        Fit f;
+        if (!fit_address(ae, t, sp.M, sp.N, sp.batch, f, why)) fail("epilogue operand '", ae.tensor, "': ", why);
+        o.ptr = t.data;
+        o.dtype = t.dtype;
+        o.a = to_addr(f);
+      }
+    }
+    {
+      const tm_tensor& t = lookup(env, sp.out.tensor);
+      Fit f;
+      if (!fit_address(sp.out, t, sp.M, sp.N, sp.batch, f, why)) fail("output '", sp.out.tensor, "': ", why);
+      p.out = t.data;
+      p.out_dtype = t.dtype;
+      p.out_a = to_addr(f);
+    }
+    if (const char* sw = std::getenv("TMB_MN_SWAP")) p.mn_lbo_sbo_swap = std::atoi(sw);
+    int grid = plan.cfg.grid > 0 ? std::min(plan.cfg.grid, sms * 4) : sms;
+    int used = grid;
+    p.tile_map = tile_mapping(sp.batch, p.tiles_m, p.tiles_n, grid, plan.cfg.raster, used);
+    k.grid = used;
+    ex->kernels.push_back(k);
+  }
+  return ex;
+}
+
+}  // namespace tmb

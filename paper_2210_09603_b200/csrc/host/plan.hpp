@@ -1,0 +1,101 @@
+// Internal planner types: a DAG partitioned into fused subgraphs, each lowered
+// to one task-mapped GEMM launch with prologue loaders and an epilogue program.
+#pragma once
+#include <map>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../device/gemm_params.h"
+#include "taskmap/ir.hpp"
+#include "taskmap/schedule.hpp"
+#include "taskmap_b200.h"
+
+namespace tmb {
+
+// Integer index program compiled from an Expr (postfix), evaluated at plan
+// bind time to fit operand/output address maps.  Variables: slot 0 = GEMM
+// row, 1 = GEMM col (or K for operands), 2 = batch.
+struct IndexProgram {
+  struct Ins {
+    int op;  // 0 imm, 1 var, 2 binary, 3 neg, 4 select
+    int64_t v;
+    taskmap::BinOp bop;
+  };
+  std::vector<Ins> code;
+  static IndexProgram compile(const taskmap::Expr& e, const std::vector<std::string>& slots);
+  int64_t eval(const int64_t* vars) const;
+};
+
+// physical tensor address as sum_d stride_d * idx_d(row, x, batch)
+struct AddrExpr {
+  std::string tensor;                    // bound tensor name
+  std::vector<taskmap::Expr> idx;        // per tensor dim, in slot vars
+  std::vector<IndexProgram> prog;        // compiled idx
+};
+
+struct ConvInfo {
+  int64_t n, c, h, w, f, kh, kw, stride, pad, ho, wo;
+  std::string x_tensor, w_tensor;
+};
+
+struct OperandPlan {
+  enum Kind { Strided, Im2col, ConvFilter } kind = Strided;
+  AddrExpr addr;  // Strided: physical idx in (row, k, batch)
+  ConvInfo conv;  // Im2col / ConvFilter
+};
+
+struct EpiStep {
+  int32_t kind;   // tmb::EpiKind
+  float c = 0.f;
+  int side = -1;  // index into SubgraphPlan::sides for *_T kinds
+};
+
+struct SubgraphPlan {
+  taskmap::FusedSubgraph sg;
+  int64_t M = 0, N = 0, K = 0, batch = 1;
+  OperandPlan a, b;                 // A provides rows, B provides cols
+  std::vector<EpiStep> ops;
+  std::vector<AddrExpr> sides;      // side operands, idx in (row, col, batch)
+  AddrExpr out;                     // output address, idx in (row, col, batch)
+  std::string describe() const;
+};
+
+struct Plan {
+  taskmap::ComputeDAG dag;
+  taskmap::ScheduleConfig cfg;
+  int device = 0;
+  std::vector<SubgraphPlan> kernels;
+  std::vector<std::string> intermediates;  // materialised between kernels
+};
+
+std::unique_ptr<Plan> build_plan(const taskmap::ComputeDAG& dag, const taskmap::ScheduleConfig& cfg,
+                                 int device);
+
+// A plan bound to tensors: fully formed kernel parameter blocks.
+struct BoundKernel {
+  GemmParams p;
+  int bn = 128, stages = 4, tf32 = 0, grid = 148, simt = 0;
+  alignas(64) unsigned char tma_a[128];
+  alignas(64) unsigned char tma_b[128];
+};
+
+struct Exec {
+  std::vector<BoundKernel> kernels;
+  std::vector<void*> scratch;  // device buffers owned by the exec
+  ~Exec();
+};
+
+std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n_in,
+                                const tm_tensor* outputs, int n_out);
+
+// kernel launcher (gemm_launch.cu)
+int num_sms(int device);
+void launch_bound(const BoundKernel& k, void* stream);
+void make_tma_2d3d(void* map, const void* ptr, int dtype, int rank, const uint64_t* dims,
+                   const uint64_t* strides_bytes, const uint32_t* box);
+void make_tma_im2col(void* map, const void* ptr, int dtype, const uint64_t* dims_cwhn,
+                     const uint64_t* strides_bytes, int pad_lo, int pad_hi_corner, int stride,
+                     uint32_t channels, uint32_t pixels);
+
+}  // namespace tmb

@@ -1,0 +1,74 @@
+// Hardware-centric schedule space for the sm_100a GEMM template
+// (§4.3: "agnostic to input size", < 200 schedules).
+#include <sstream>
+
+#include "json.hpp"
+#include "taskmap/schedule.hpp"
+
+namespace taskmap {
+
+std::string ScheduleConfig::to_json() const {
+  std::ostringstream o;
+  o << "{\"block_m\":" << block_m << ",\"block_n\":" << block_n << ",\"block_k\":" << block_k
+    << ",\"warp_m\":" << warp_m << ",\"warp_n\":" << warp_n << ",\"threads_per_block\":" << threads_per_block
+    << ",\"pipeline\":" << (pipeline ? "true" : "false") << ",\"split_k\":" << split_k
+    << ",\"stages\":" << stages << ",\"raster\":" << raster << ",\"grid\":" << grid
+    << ",\"math\":" << tmjson::quote(math) << "}";
+  return o.str();
+}
+
+ScheduleConfig ScheduleConfig::from_json(const std::string& text) {
+  ScheduleConfig c;
+  tmjson::Value v;
+  try {
+    v = tmjson::parse(text);
+  } catch (const std::exception& e) {
+    fail(e.what());
+  }
+  auto geti = [&](const char* k, int& dst) {
+    if (const auto* x = v.get(k)) dst = static_cast<int>(x->integer());
+  };
+  geti("block_m", c.block_m);
+  geti("block_n", c.block_n);
+  geti("block_k", c.block_k);
+  geti("warp_m", c.warp_m);
+  geti("warp_n", c.warp_n);
+  geti("threads_per_block", c.threads_per_block);
+  geti("split_k", c.split_k);
+  geti("stages", c.stages);
+  geti("raster", c.raster);
+  geti("grid", c.grid);
+  if (const auto* x = v.get("pipeline")) c.pipeline = x->type == tmjson::Value::Bool ? x->b : x->integer() != 0;
+  if (const auto* x = v.get("math")) c.math = x->str();
+  return c;
+}
+
+std::string ScheduleConfig::key() const {
+  std::ostringstream o;
+  o << "bn" << block_n << (pipeline ? "_deep" : "_db") << "_r" << raster << "_sk" << split_k << "_" << math;
+  return o.str();
+}
+
+// The space: UMMA N (tile width; M is fixed at 128 TMEM lanes) x ring depth
+// (paper double buffer = 2 stages, or the deepest ring that fits 227 KB) x
+// CTA->tile task mapping (repeat*spatial vs spatial*repeat).  The same list is
+// returned for every problem shape; tails are handled by TMA zero fill and
+// predicated gathers/stores, never by shrinking the space.
+std::vector<ScheduleConfig> schedule_space(const std::string& op_kind) {
+  if (op_kind != "matmul" && op_kind != "conv2d" && op_kind != "batch_matmul")
+    fail("unknown op kind '", op_kind, "' for schedule_space");
+  std::vector<ScheduleConfig> out;
+  for (int bn : {128, 256, 192, 64})
+    for (bool deep : {true, false})
+      for (int raster : {0, 1}) {
+        ScheduleConfig c;
+        c.block_n = bn;
+        c.pipeline = deep;
+        c.stages = deep ? 0 : 2;
+        c.raster = raster;
+        out.push_back(c);
+      }
+  return out;
+}
+
+}  // namespace taskmap
