@@ -109,6 +109,12 @@ void tm_exec_destroy(tm_exec* e);
 tm_status tm_exec_launch(const tm_exec* e, void* cuda_stream);
 /* Number of kernel launches per tm_exec_launch. */
 int32_t tm_exec_num_launches(const tm_exec* e);
+/* Launch geometry of kernel `index`: grid size, CTAs per MMA (1/2), tile N, split-K. */
+tm_status tm_exec_kernel_info(const tm_exec* e, int32_t index, int32_t* grid, int32_t* cta_group,
+                              int32_t* block_n, int32_t* split_k, int32_t* a_loader, int32_t* b_loader);
+/* Per-tile role timeline of kernel `index` (exec created with TMB_TRACE=1 in the
+ * environment): [grid][64 tiles][8 events] int64 clock64 deltas; see TraceEv. */
+tm_status tm_exec_trace(const tm_exec* e, int32_t index, int64_t* buf, size_t cap);
 /* bind + launch (+ destroy) in one call. */
 tm_status tm_plan_launch(const tm_plan* p, const tm_tensor* inputs, int32_t n_in,
                          const tm_tensor* outputs, int32_t n_out, void* cuda_stream);

@@ -32,17 +32,39 @@ enum EpiKind : int32_t {
   EPI_RELU = 32, EPI_GELU_TANH, EPI_EXP, EPI_SQRT, EPI_NEG, EPI_ROUND_BF16
 };
 
+// How a side operand varies over the output tile (decides where the
+// epilogue keeps it): per-column vectors (bias, BN scale/shift) are staged in
+// shared memory once per tile, per-row scalars live in a register, general
+// matrices (residuals) are prefetched one 16-column chunk ahead.
+enum SideKind : int32_t { SIDE_NONE = 0, SIDE_COL = 1, SIDE_ROW = 2, SIDE_MAT = 3 };
+
 // One epilogue op; *_T kinds read a side tensor at `a` (dtype `dtype`).
 struct EpiOp {
   int32_t kind;
   int32_t dtype;
   float c;
+  int32_t side;  // SideKind
+  int32_t slot;  // SIDE_MAT: prefetch slot (< kMaxMatOps)
   int32_t pad_;
   const void* ptr;
   Addr a;
 };
 
 constexpr int kMaxEpiOps = 8;
+constexpr int kMaxMatOps = 2;
+constexpr int kTraceTiles = 64;
+constexpr int kTraceEvents = 8;
+// trace events per tile
+enum TraceEv : int32_t {
+  TR_PROD_FIRST = 0,  // producer: first k-block slot acquired
+  TR_PROD_LAST,       // producer: last TMA of the tile issued
+  TR_MMA_FIRST,       // MMA: first k-block data ready
+  TR_MMA_LAST,        // MMA: last MMA issued / commit
+  TR_EPI_READY,       // epilogue: column operands staged
+  TR_EPI_ACC,         // epilogue: accumulator available
+  TR_EPI_DONE,        // epilogue: tile stored
+  TR_CTA_START        // (tile 0 only) CTA start, globaltimer ns
+};
 
 enum LoaderKind : int32_t {
   LD_TMA_K = 0,         // TMA tile load, K contiguous (K-major)
@@ -84,7 +106,21 @@ struct GemmParams {
   Strided a, b;
   ConvGeom conv;
   tm::DevMapping tile_map;  // CTA -> (batch, tile_m, tile_n) task mapping
+  // split-K (SPEC.md:277 split_k): work unit = (batch, k-split, tile_m, tile_n);
+  // tile_map coordinate 0 enumerates batch * split_k + ks.  Each unit covers
+  // k-blocks [ks*kb_per_split, min(num_kb, (ks+1)*kb_per_split)); partial
+  // tiles go to `workspace` (fp32) and the last unit to arrive on the tile's
+  // counter sums them in split order (deterministic) and runs the epilogue.
+  int32_t split_k;
+  int32_t kb_per_split;
+  float* workspace;
+  int32_t* counters;
+  int32_t fast_math;  // approximate transcendentals (bf16 outputs)
+  // optional per-tile role timeline (clock64 relative to CTA start), layout
+  // [cta][kTraceTiles][kTraceEvents]; null = tracing off
+  long long* trace;
   int32_t n_ops;
+  int32_t has_mat;  // any SIDE_MAT op
   int32_t out_dtype;
   EpiOp ops[kMaxEpiOps];
   void* out;

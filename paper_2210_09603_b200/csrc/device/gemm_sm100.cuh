@@ -15,8 +15,8 @@
 //     list (bias / scale / BN-fold / ReLU / GELU / residual ...) and store
 //     through the epilogue's output address map (NCHW re-index etc.).
 //
-// Warp roles (9 warps): 0-3 loaders, 4-7 epilogue (TMEM lane groups 0-3),
-// 8 MMA issuer + TMEM owner.
+// Warp roles (13 warps): 0-3 loaders, 4-11 epilogue (TMEM lane group = warp%4,
+// interleaved 16-column chunks), 12 MMA issuer + TMEM owner.
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -28,26 +28,41 @@ namespace tmb {
 
 constexpr int kBM = 128;          // tile rows (TMEM lanes)
 constexpr int kRowBytes = 128;    // one swizzle-128B row of K
-constexpr int kNumThreads = 288;  // 9 warps
+constexpr int kEpiWarps = 8;       // epilogue warps (2 per TMEM lane group)
+constexpr int kNumThreads = 32 * (4 + kEpiWarps + 1);  // loaders + epilogue + MMA
 
-template <int BN, int STAGES, bool TF32>
+// CG = CTAs per MMA (cta_group): 1, or 2 for the SM-pair form where the tile
+// is (2*128) x BN, each CTA stages its 128 rows of A and BN/2 rows of B, and
+// the pair leader issues tcgen05.mma.cta_group::2 over both CTAs' smem.
+template <int BN, int STAGES, bool TF32, int CG = 1>
 struct GemmCfg {
   static constexpr int kElem = TF32 ? 4 : 2;
   static constexpr int BK = kRowBytes / kElem;        // 64 bf16 / 32 tf32
   static constexpr int KSTEP = TF32 ? 8 : 16;          // K per tcgen05.mma
   static constexpr int NSTEP = BK / KSTEP;             // 4
   static constexpr int A_BYTES = kBM * kRowBytes;      // 16 KB
-  static constexpr int B_BYTES = BN * kRowBytes;
+  static constexpr int B_BYTES = (BN / CG) * kRowBytes;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int COLBUF_BYTES = kMaxEpiOps * BN * 4;  // staged per-column epilogue operands
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + COLBUF_BYTES;
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 must be 16..256 step 16");
 };
 
 namespace detail {
 
 __device__ __forceinline__ int64_t addr_rowpart(const Addr& a, int64_t row, int64_t batch) {
-  return (row / a.P) * a.s_hi + (row % a.P) * a.s_lo + batch * a.s_batch + a.offset;
+  int64_t q, r;
+  if (a.P < (int64_t(1) << 31) && row < (int64_t(1) << 31)) {  // 32-bit divide fast path
+    const uint32_t rr = static_cast<uint32_t>(row), pp = static_cast<uint32_t>(a.P);
+    const uint32_t qq = rr / pp;
+    q = qq;
+    r = rr - qq * pp;
+  } else {
+    q = row / a.P;
+    r = row % a.P;
+  }
+  return q * a.s_hi + r * a.s_lo + batch * a.s_batch + a.offset;
 }
 
 // Raw bits of one element converted to the MMA input format.
@@ -197,10 +212,24 @@ __device__ __forceinline__ void gather_row_filter(uint8_t* tile, int r, const Co
 }
 
 __device__ __forceinline__ float gelu_tanh(float x) {
-  // 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))), tanh(u) = 1 - 2/(exp(2u)+1)
+  // 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))), tanh(u) = 1 - 2/(exp(2u)+1);
+  // __fdividef(2, inf) = 0 gives the right limit when exp overflows.
   const float u = 0.7978845608028654f * (x + 0.044715f * x * x * x);
-  const float t = 1.0f - 2.0f / (__expf(2.0f * u) + 1.0f);
+  const float t = 1.0f - __fdividef(2.0f, __expf(2.0f * u) + 1.0f);
   return 0.5f * x * (1.0f + t);
+}
+
+__device__ __forceinline__ float tanh_approx(float x) {
+  float y;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// one MUFU op per element; used when the output is bf16 (|err| ~ 2^-11 << bf16 ulp)
+__device__ __forceinline__ float gelu_tanh_fast(float x) {
+  const float u = 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
+  const float hx = 0.5f * x;
+  return fmaf(hx, tanh_approx(u), hx);
 }
 
 __device__ __forceinline__ float load_side(const void* p, int64_t idx, int32_t dt) {
@@ -209,38 +238,88 @@ __device__ __forceinline__ float load_side(const void* p, int64_t idx, int32_t d
   return __half2float(reinterpret_cast<const __half*>(p)[idx]);
 }
 
+__device__ __forceinline__ void bf16x8_to_f32(const uint4 u, float* o) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    o[2 * i] = __uint_as_float(w[i] << 16);
+    o[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+
+// 16 consecutive columns of a matrix side operand for one row (vectorised
+// when contiguous and 16-byte aligned, otherwise predicated scalar loads).
+__device__ __forceinline__ void load_mat16(const EpiOp& op, int64_t rowpart, int64_t col0, int N,
+                                           bool row_ok, float (&out)[16]) {
+  if (!row_ok) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) out[j] = 0.f;
+    return;
+  }
+  const int64_t base = rowpart + col0 * op.a.s_col;
+  if (op.a.s_col == 1 && col0 + 16 <= N) {
+    if (op.dtype == DT_BF16 && ((reinterpret_cast<uintptr_t>(op.ptr) + base * 2) & 15) == 0) {
+      const uint4* q = reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(op.ptr) + base);
+      bf16x8_to_f32(__ldg(q), out);
+      bf16x8_to_f32(__ldg(q + 1), out + 8);
+      return;
+    }
+    if (op.dtype == DT_F32 && ((reinterpret_cast<uintptr_t>(op.ptr) + base * 4) & 15) == 0) {
+      const float4* q = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(op.ptr) + base);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 f = __ldg(q + i);
+        out[4 * i] = f.x; out[4 * i + 1] = f.y; out[4 * i + 2] = f.z; out[4 * i + 3] = f.w;
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    out[j] = (col0 + j < N) ? load_side(op.ptr, base + j * op.a.s_col, op.dtype) : 0.f;
+}
+
 // Applies the fused epilogue op list to 16 consecutive columns of one row.
-__device__ __forceinline__ void apply_epilogue(const GemmParams& p, float (&v)[16],
-                                               const int64_t* rowpart, int64_t col0,
-                                               bool row_ok) {
+// Side operands come from: smem column buffers (SIDE_COL), a per-row register
+// (SIDE_ROW) or the prefetched matrix chunk (SIDE_MAT).
+template <int BN>
+__device__ __forceinline__ void apply_epilogue(const GemmParams& p, float (&v)[16], const float* colbuf,
+                                               int cbase, const float* rowv, const float (&mat)[kMaxMatOps][16]) {
   for (int o = 0; o < p.n_ops; ++o) {
     const EpiOp& op = p.ops[o];
     const int kind = op.kind;
     if (kind >= EPI_ADD_T && kind <= EPI_MIN_T) {
       float s[16];
-      if (op.a.s_col == 0) {
-        const float x = row_ok ? load_side(op.ptr, rowpart[o], op.dtype) : 0.f;
+      if (op.side == SIDE_COL) {
+        const float4* cb = reinterpret_cast<const float4*>(colbuf + o * BN + cbase);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float4 f = cb[i];
+          s[4 * i] = f.x; s[4 * i + 1] = f.y; s[4 * i + 2] = f.z; s[4 * i + 3] = f.w;
+        }
+      } else if (op.side == SIDE_ROW) {
+        const float x = rowv[o];
 #pragma unroll
         for (int j = 0; j < 16; ++j) s[j] = x;
       } else {
+        const int sl = op.slot;
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          s[j] = (row_ok && col0 + j < p.N)
-                     ? load_side(op.ptr, rowpart[o] + (col0 + j) * op.a.s_col, op.dtype)
-                     : 0.f;
+        for (int j = 0; j < 16; ++j) s[j] = sl == 0 ? mat[0][j] : mat[1][j];
       }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        switch (kind) {
-          case EPI_ADD_T: v[j] = v[j] + s[j]; break;
-          case EPI_SUB_T: v[j] = v[j] - s[j]; break;
-          case EPI_RSUB_T: v[j] = s[j] - v[j]; break;
-          case EPI_MUL_T: v[j] = v[j] * s[j]; break;
-          case EPI_DIV_T: v[j] = v[j] / s[j]; break;
-          case EPI_RDIV_T: v[j] = s[j] / v[j]; break;
-          case EPI_MAX_T: v[j] = fmaxf(v[j], s[j]); break;
-          default: v[j] = fminf(v[j], s[j]); break;
-        }
+      switch (kind) {
+#define TMB_TW(K, EXPR) \
+  case K:               \
+    _Pragma("unroll") for (int j = 0; j < 16; ++j) { const float x = v[j], y = s[j]; v[j] = (EXPR); } break;
+        TMB_TW(EPI_ADD_T, x + y)
+        TMB_TW(EPI_SUB_T, x - y)
+        TMB_TW(EPI_RSUB_T, y - x)
+        TMB_TW(EPI_MUL_T, x * y)
+        TMB_TW(EPI_DIV_T, x / y)
+        TMB_TW(EPI_RDIV_T, y / x)
+        TMB_TW(EPI_MAX_T, fmaxf(x, y))
+        TMB_TW(EPI_MIN_T, fminf(x, y))
+#undef TMB_TW
+        default: break;
       }
       continue;
     }
@@ -258,7 +337,7 @@ __device__ __forceinline__ void apply_epilogue(const GemmParams& p, float (&v)[1
       TMB_EW(EPI_MAX_C, fmaxf(x, c))
       TMB_EW(EPI_MIN_C, fminf(x, c))
       TMB_EW(EPI_RELU, fmaxf(x, 0.f))
-      TMB_EW(EPI_GELU_TANH, gelu_tanh(x))
+      TMB_EW(EPI_GELU_TANH, p.fast_math ? gelu_tanh_fast(x) : gelu_tanh(x))
       TMB_EW(EPI_EXP, __expf(x))
       TMB_EW(EPI_SQRT, sqrtf(x))
       TMB_EW(EPI_NEG, -x)
@@ -312,12 +391,19 @@ __device__ __forceinline__ void store_out(const GemmParams& p, const float (&v)[
 
 // Decodes task `i` of this CTA into (batch, tile_m, tile_n); false once the
 // CTA's task list is exhausted.  Out-of-range tasks are reported via `valid`.
-__device__ __forceinline__ bool next_tile(const GemmParams& p, uint32_t i, int& b, int& tm_,
+__device__ __forceinline__ void trace(const GemmParams& p, uint32_t i, int ev, long long t0) {
+  if (p.trace != nullptr && i < static_cast<uint32_t>(kTraceTiles))
+    p.trace[(static_cast<int64_t>(blockIdx.x) * kTraceTiles + i) * kTraceEvents + ev] = clock64() - t0;
+}
+
+template <int CG>
+__device__ __forceinline__ bool next_tile(const GemmParams& p, uint32_t i, int& b, int& ks, int& tm_,
                                           int& tn, bool& valid) {
   if (i >= p.tile_map.tasks) return false;
   int32_t c[tm::kMaxRank];
-  tm::dev_task(p.tile_map, blockIdx.x, i, c);
-  b = c[0];
+  tm::dev_task(p.tile_map, blockIdx.x / CG, i, c);  // workers = CTA pairs when CG == 2
+  b = c[0] / p.split_k;
+  ks = c[0] % p.split_k;
   tm_ = c[1];
   tn = c[2];
   valid = b < p.batch && tm_ < p.tiles_m && tn < p.tiles_n;
@@ -326,12 +412,14 @@ __device__ __forceinline__ bool next_tile(const GemmParams& p, uint32_t i, int& 
 
 }  // namespace detail
 
-template <int BN, int STAGES, bool TF32>
+template <int BN, int STAGES, bool TF32, int CG>
 __global__ void __launch_bounds__(kNumThreads, 1)
     tm_gemm_kernel(const __grid_constant__ GemmParams p, const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB) {
-  using Cfg = GemmCfg<BN, STAGES, TF32>;
+  using Cfg = GemmCfg<BN, STAGES, TF32, CG>;
   constexpr int BK = Cfg::BK;
+  constexpr int kTileM = kBM * CG;  // rows per tile (both CTAs of a pair)
+  const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0u;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = ptx::smem_u32(smem_raw);
   uint8_t* smem = smem_raw + ((1024u - (raw & 1023u)) & 1023u);
@@ -342,6 +430,8 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint32_t* split_flag = tmem_slot + 1;
+  float* colbuf = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -358,15 +448,23 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 4);
+      ptx::mbar_init(&tempty[a], kEpiWarps * CG);  // both CTAs' epilogues drain before reuse
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 8) ptx::tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  if (warp == 4 + kEpiWarps) {
+    if constexpr (CG == 2) ptx::tmem_alloc_2sm<Cfg::TMEM_COLS>(tmem_slot);
+    else ptx::tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
+  }
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2) ptx::cluster_sync();  // peer barriers initialised before any TMA/arrive
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const long long t0 = clock64();
+  if (p.trace != nullptr && threadIdx.x == 0)
+    p.trace[static_cast<int64_t>(blockIdx.x) * kTraceTiles * kTraceEvents + TR_CTA_START] =
+        static_cast<long long>(ptx::globaltimer());
 
   if (warp < 4) {
     // ===================== loaders (prologue splice) =====================
@@ -376,16 +474,47 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     } else {
       int stage = 0;
       uint32_t phase = 0;
-      int b, tm_, tn;
+      int b, ks, tm_, tn;
       bool valid;
-      for (uint32_t i = 0; detail::next_tile(p, i, b, tm_, tn, valid); ++i) {
+      for (uint32_t i = 0; detail::next_tile<CG>(p, i, b, ks, tm_, tn, valid); ++i) {
         if (!valid) continue;
-        const int m0 = tm_ * kBM, n0 = tn * BN;
-        for (int kb = 0; kb < p.num_kb; ++kb) {
-          ptx::mbar_wait(&empty[stage], phase ^ 1u);
+        // this CTA's rows of A and columns of B (half of each tile's B when CG == 2)
+        const int m0 = tm_ * kTileM + rank * kBM, n0 = tn * BN + rank * (BN / CG);
+        for (int kb0 = ks * p.kb_per_split, kb = kb0, kb_end = min(p.num_kb, kb0 + p.kb_per_split); kb < kb_end; ++kb) {
+          if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&empty[stage], phase ^ 1u);
+          else ptx::mbar_wait(&empty[stage], phase ^ 1u);
+          if (kb == kb0 && t == 0) detail::trace(p, i, TR_PROD_FIRST, t0);
+          if (kb == kb_end - 1 && t == 0) detail::trace(p, i, TR_PROD_LAST, t0);
           uint8_t* a_tile = smA + stage * Cfg::A_BYTES;
           uint8_t* b_tile = smB + stage * Cfg::B_BYTES;
           const int k0 = kb * BK;
+          if constexpr (CG == 2) {
+            // both CTAs' TMA bytes complete on the leader's full barrier
+            const uint32_t lead_full = ptx::mapa_shared(ptx::smem_u32(&full[stage]), 0);
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], CG * Cfg::STAGE_BYTES);
+            if (p.a_loader == LD_TMA_K) {
+              ptx::tma_load_3d_2sm(a_tile, &tmA, lead_full, k0, m0, b);
+            } else {
+              const int cblocks = p.conv.c / BK;
+              const int tap = kb / cblocks, cb = kb % cblocks;
+              const int fh = tap / p.conv.kw, fw = tap % p.conv.kw;
+              const int hw = p.conv.ho * p.conv.wo;
+              const int img = m0 / hw, rem = m0 % hw;
+              const int oh = rem / p.conv.wo, ow = rem % p.conv.wo;
+              ptx::tma_load_im2col_4d_2sm(a_tile, &tmA, lead_full, cb * BK, ow * p.conv.stride - p.conv.pad,
+                                          oh * p.conv.stride - p.conv.pad, img, static_cast<uint16_t>(fw),
+                                          static_cast<uint16_t>(fh));
+            }
+            if (p.b_loader == LD_TMA_K) {
+              ptx::tma_load_3d_2sm(b_tile, &tmB, lead_full, k0, n0, b);
+            } else {
+#pragma unroll 1
+              for (int j = 0; j < BN / CG / 64; ++j)
+                ptx::tma_load_3d_2sm(b_tile + j * (64 * kRowBytes), &tmB, lead_full, n0 + 64 * j, k0, b);
+            }
+            if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+            continue;
+          }
           if (all_tma) {
             ptx::mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
           } else if (t == 0) {
@@ -446,63 +575,167 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
       }
     }
-  } else if (warp < 8) {
+  } else if (warp < 4 + kEpiWarps) {
     // ===================== epilogue (epilogue splice) =====================
-    const int lg = warp - 4;  // TMEM lane group
+    const int e = warp - 4;          // 0..7
+    const int lg = warp & 3;         // TMEM lane group this warp may access
+    const int half = e >> 2;         // which interleaved half of the 16-column chunks
+    const int et = threadIdx.x - 128;
+    constexpr int kChunks = BN / 16;
     int acc = 0;
     uint32_t acc_phase = 0;
-    int b, tm_, tn;
+    int b, ks, tm_, tn;
     bool valid;
     int64_t rowpart[kMaxEpiOps];
-    for (uint32_t i = 0; detail::next_tile(p, i, b, tm_, tn, valid); ++i) {
+    float rowv[kMaxEpiOps];
+    for (uint32_t i = 0; detail::next_tile<CG>(p, i, b, ks, tm_, tn, valid); ++i) {
       if (!valid) continue;
-      ptx::mbar_wait(&tfull[acc], acc_phase);
-      ptx::tc_fence_after();
-      const int64_t row = static_cast<int64_t>(tm_) * kBM + lg * 32 + lane;
+      const int64_t n0 = static_cast<int64_t>(tn) * BN;
+      const int64_t row = static_cast<int64_t>(tm_) * kTileM + rank * kBM + lg * 32 + lane;
       const bool row_ok = row < p.M;
       const int64_t rr = row_ok ? row : 0;
-      for (int o = 0; o < p.n_ops; ++o) rowpart[o] = detail::addr_rowpart(p.ops[o].a, rr, b);
+      // stage this tile's column vectors while the MMA works on it
+      ptx::named_bar_sync(1, 32 * kEpiWarps);  // previous tile's readers are done
+      for (int o = 0; o < p.n_ops; ++o) {
+        const EpiOp& op = p.ops[o];
+        rowpart[o] = detail::addr_rowpart(op.a, rr, b);
+        if (op.side == SIDE_COL) {
+          const int64_t cb = detail::addr_rowpart(op.a, 0, b);
+          for (int c = et; c < BN; c += 32 * kEpiWarps)
+            colbuf[o * BN + c] = (n0 + c < p.N) ? detail::load_side(op.ptr, cb + (n0 + c) * op.a.s_col, op.dtype) : 0.f;
+        } else if (op.side == SIDE_ROW) {
+          rowv[o] = row_ok ? detail::load_side(op.ptr, rowpart[o], op.dtype) : 0.f;
+        }
+      }
       const int64_t obase = detail::addr_rowpart(p.out_a, rr, b);
+      ptx::named_bar_sync(1, 32 * kEpiWarps);  // column buffers ready
+      if (et == 0) detail::trace(p, i, TR_EPI_READY, t0);
+      float mat[kMaxMatOps][16];
+      auto prefetch = [&](int c, float (&dst)[kMaxMatOps][16]) {
+        for (int o = 0; o < p.n_ops; ++o)
+          if (p.ops[o].side == SIDE_MAT) {
+            float tmp[16];
+            detail::load_mat16(p.ops[o], rowpart[o], n0 + c * 16, p.N, row_ok, tmp);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (p.ops[o].slot == 0) dst[0][j] = tmp[j];
+              else dst[1][j] = tmp[j];
+            }
+          }
+      };
+      if (p.has_mat) prefetch(half, mat);
+      if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&tfull[acc], acc_phase);
+      else ptx::mbar_wait(&tfull[acc], acc_phase);
+      ptx::tc_fence_after();
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lg * 32) << 16) + acc * BN;
+      if (et == 0) detail::trace(p, i, TR_EPI_ACC, t0);
+      if (p.split_k > 1) {
+        // ---- split-K: park the raw partial tile, last unit reduces + runs the epilogue
+        const int64_t tile_id = ((static_cast<int64_t>(b) * p.tiles_m + tm_) * p.tiles_n + tn) * CG + rank;
+        const float* ws = p.workspace + tile_id * p.split_k * static_cast<int64_t>(kBM * BN);
+        const int rloc = lg * 32 + lane;
 #pragma unroll 1
-      for (int c = 0; c < BN / 16; ++c) {
-        const int64_t col0 = static_cast<int64_t>(tn) * BN + c * 16;
+        for (int c = half; c < kChunks; c += 2) {
+          uint32_t r[16];
+          ptx::tmem_ld16(taddr + c * 16, r);
+          ptx::tmem_wait_ld();
+          // chunk-major layout: a warp writes 32 consecutive 64-byte rows
+          float4* dst = reinterpret_cast<float4*>(const_cast<float*>(ws) + ks * static_cast<int64_t>(kBM * BN) +
+                                                  (static_cast<int64_t>(c) * kBM + rloc) * 16);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            __stcg(dst + q, make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                        __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {  // TMEM is free again: the MMA can start the next unit
+          if constexpr (CG == 2) ptx::mbar_arrive_remote(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
+          else ptx::mbar_arrive(&tempty[acc]);
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+        __threadfence();
+        ptx::named_bar_sync(2, 32 * kEpiWarps);
+        if (et == 0) *split_flag = (atomicAdd(&p.counters[tile_id], 1) == p.split_k - 1) ? 1u : 0u;
+        ptx::named_bar_sync(2, 32 * kEpiWarps);
+        if (*reinterpret_cast<volatile uint32_t*>(split_flag) == 0u) continue;
+        __threadfence();
+#pragma unroll 1
+        for (int c = half; c < kChunks; c += 2) {
+          const int64_t col0 = n0 + c * 16;
+          if (col0 >= p.N) break;
+          if (p.has_mat) prefetch(c, mat);
+          float v[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = 0.f;
+          for (int s = 0; s < p.split_k; ++s) {  // fixed order: deterministic
+            const float4* src = reinterpret_cast<const float4*>(ws + s * static_cast<int64_t>(kBM * BN) +
+                                                                (static_cast<int64_t>(c) * kBM + rloc) * 16);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 f = __ldcg(src + q);
+              v[4 * q] += f.x; v[4 * q + 1] += f.y; v[4 * q + 2] += f.z; v[4 * q + 3] += f.w;
+            }
+          }
+          detail::apply_epilogue<BN>(p, v, colbuf, c * 16, rowv, mat);
+          detail::store_out(p, v, obase, col0, row_ok);
+        }
+        if (et == 0) p.counters[tile_id] = 0;  // self-resetting for the next launch
+        continue;
+      }
+#pragma unroll 1
+      for (int c = half; c < kChunks; c += 2) {
+        const int64_t col0 = n0 + c * 16;
         if (col0 >= p.N) break;  // warp-uniform
+        float nxt[kMaxMatOps][16];
+        if (p.has_mat && c + 2 < kChunks && col0 + 32 < p.N + 16) prefetch(c + 2, nxt);
         uint32_t r[16];
         ptx::tmem_ld16(taddr + c * 16, r);
         ptx::tmem_wait_ld();
         float v[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-        detail::apply_epilogue(p, v, rowpart, col0, row_ok);
+        detail::apply_epilogue<BN>(p, v, colbuf, c * 16, rowv, mat);
         detail::store_out(p, v, obase, col0, row_ok);
+        if (p.has_mat) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) { mat[0][j] = nxt[0][j]; mat[1][j] = nxt[1][j]; }
+        }
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+      if (lane == 0) {
+        // the (leader's) MMA may overwrite this accumulator once both CTAs drained it
+        if constexpr (CG == 2) ptx::mbar_arrive_remote(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
+        else ptx::mbar_arrive(&tempty[acc]);
+      }
+      if (et == 0) detail::trace(p, i, TR_EPI_DONE, t0);
       if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
     }
   } else {
     // ===================== MMA issuer (single thread) =====================
-    if (lane == 0) {
+    if (lane == 0 && rank == 0) {
       const bool b_mn = p.b_loader == LD_TMA_MN;
-      const uint32_t idesc = ptx::make_idesc(kBM, BN, TF32 ? 2u : 1u, false, b_mn);
+      const uint32_t idesc = ptx::make_idesc(kTileM, BN, TF32 ? 2u : 1u, false, b_mn);
       const uint32_t mn_lbo = p.mn_lbo_sbo_swap ? 1024u : 64u * kRowBytes;
       const uint32_t mn_sbo = p.mn_lbo_sbo_swap ? 64u * kRowBytes : 1024u;
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      int b, tm_, tn;
+      int b, ks, tm_, tn;
       bool valid;
-      for (uint32_t i = 0; detail::next_tile(p, i, b, tm_, tn, valid); ++i) {
+      for (uint32_t i = 0; detail::next_tile<CG>(p, i, b, ks, tm_, tn, valid); ++i) {
         if (!valid) continue;
-        ptx::mbar_wait(&tempty[acc], acc_phase ^ 1u);
+        if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&tempty[acc], acc_phase ^ 1u);
+        else ptx::mbar_wait(&tempty[acc], acc_phase ^ 1u);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BN;
-        for (int kb = 0; kb < p.num_kb; ++kb) {
-          ptx::mbar_wait(&full[stage], phase);
+        for (int kb0 = ks * p.kb_per_split, kb = kb0, kb_end = min(p.num_kb, kb0 + p.kb_per_split); kb < kb_end; ++kb) {
+          if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&full[stage], phase);
+          else ptx::mbar_wait(&full[stage], phase);
           ptx::tc_fence_after();
+          if (kb == kb0) detail::trace(p, i, TR_MMA_FIRST, t0);
           const uint32_t a_addr = ptx::smem_u32(smA + stage * Cfg::A_BYTES);
           const uint32_t b_addr = ptx::smem_u32(smB + stage * Cfg::B_BYTES);
 #pragma unroll
@@ -511,24 +744,35 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             const uint64_t bdesc =
                 b_mn ? ptx::smem_desc_sw128(b_addr + kk * Cfg::KSTEP * kRowBytes, mn_lbo, mn_sbo)
                      : ptx::smem_desc_sw128(b_addr + kk * Cfg::KSTEP * Cfg::kElem, 16, 1024);
-            const uint32_t accum = (kb | kk) != 0;
-            if (TF32) ptx::mma_tf32(d_tmem, adesc, bdesc, idesc, accum);
-            else ptx::mma_f16(d_tmem, adesc, bdesc, idesc, accum);
+            const uint32_t accum = (kb != kb0 || kk != 0);
+            if constexpr (CG == 2) {
+              if (TF32) ptx::mma_tf32_2sm(d_tmem, adesc, bdesc, idesc, accum);
+              else ptx::mma_f16_2sm(d_tmem, adesc, bdesc, idesc, accum);
+            } else {
+              if (TF32) ptx::mma_tf32(d_tmem, adesc, bdesc, idesc, accum);
+              else ptx::mma_f16(d_tmem, adesc, bdesc, idesc, accum);
+            }
           }
-          ptx::mma_commit(&empty[stage]);
+          // frees this ring slot in both CTAs of the pair
+          if constexpr (CG == 2) ptx::mma_commit_2sm(&empty[stage], 0x3);
+          else ptx::mma_commit(&empty[stage]);
           if (++stage == STAGES) { stage = 0; phase ^= 1u; }
         }
-        ptx::mma_commit(&tfull[acc]);
+        if constexpr (CG == 2) ptx::mma_commit_2sm(&tfull[acc], 0x3);
+        else ptx::mma_commit(&tfull[acc]);
+        detail::trace(p, i, TR_MMA_LAST, t0);
         if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
       }
     }
   }
 
   ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 8) {
+  if constexpr (CG == 2) ptx::cluster_sync();  // peer done with its TMEM before the pair frees it
+  else __syncthreads();
+  if (warp == 4 + kEpiWarps) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+    if constexpr (CG == 2) ptx::tmem_dealloc_2sm<Cfg::TMEM_COLS>(tmem_base);
+    else ptx::tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
   }
 }
 

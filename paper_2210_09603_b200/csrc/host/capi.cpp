@@ -311,6 +311,33 @@ tm_status tm_exec_launch(const tm_exec* e, void* stream) {
 
 int32_t tm_exec_num_launches(const tm_exec* e) { return e ? static_cast<int32_t>(e->e->kernels.size()) : 0; }
 
+tm_status tm_exec_kernel_info(const tm_exec* e, int32_t index, int32_t* grid, int32_t* cg, int32_t* bn, int32_t* sk,
+                              int32_t* al, int32_t* bl) {
+  return guarded([&] {
+    if (!e || index < 0 || index >= static_cast<int32_t>(e->e->kernels.size())) fail("bad kernel index");
+    const auto& k = e->e->kernels[index];
+    if (grid) *grid = k.grid;
+    if (cg) *cg = k.cg;
+    if (bn) *bn = k.bn;
+    if (sk) *sk = k.p.split_k;
+    if (al) *al = k.p.a_loader;
+    if (bl) *bl = k.p.b_loader;
+    return TM_OK;
+  });
+}
+
+tm_status tm_exec_trace(const tm_exec* e, int32_t index, int64_t* buf, size_t cap) {
+  return guarded([&] {
+    if (!e || index < 0 || index >= static_cast<int32_t>(e->e->kernels.size())) fail("bad kernel index");
+    const auto& k = e->e->kernels[index];
+    if (!k.p.trace) fail("exec was not created with TMB_TRACE set");
+    const size_t n = size_t(k.grid) * tmb::kTraceTiles * tmb::kTraceEvents;
+    if (cap < n) fail("trace buffer too small: need ", n);
+    if (cudaMemcpy(buf, k.p.trace, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) fail("cuda memcpy failed");
+    return TM_OK;
+  });
+}
+
 tm_status tm_plan_launch(const tm_plan* p, const tm_tensor* in, int32_t n_in, const tm_tensor* out, int32_t n_out,
                          void* stream) {
   return guarded([&] {

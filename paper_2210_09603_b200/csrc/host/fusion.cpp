@@ -431,12 +431,25 @@ SubgraphPlan lower_subgraph(const ComputeDAG& dag, const FusedSubgraph& sg) {
     for (const auto& i : ld->args) idx.push_back(substitute(i, ren));
     const TensorNode& s = dag.at(ld->name);
     const bool is_pro = (which == 0 ? pro0 : pro1);
+    // Pure re-index prologue (value = Load of a graph input): compose its
+    // index expressions with the anchor's access by substitution.  Kept even
+    // for recognised conv operands: when the bound strides make it a plain
+    // TMA tile (1x1 stride-1 conv on channels-last data) it beats im2col.
+    auto reindex = [&](AddrExpr& out) {
+      if (s.value->kind != ExprKind::Load || dag.at(s.value->name).kind != NodeKind::Input) return false;
+      std::map<std::string, Expr> sub_map;
+      for (size_t d = 0; d < s.axes.size(); ++d) sub_map[s.axes[d].name] = idx[d];
+      out.tensor = s.value->name;
+      for (const auto& i : s.value->args) out.idx.push_back(fold(substitute(i, sub_map)));
+      return true;
+    };
     if (which == im2col_side) {
       // the anchor must read Col[k, pixel] directly
       if (idx.size() != 2 || !expr_equal(idx[0], var(kCol)) || !expr_equal(idx[1], var(kRow)))
         fail("anchor reads the im2col node through a non-identity index");
       op.kind = OperandPlan::Im2col;
       op.conv = ci;
+      reindex(op.addr);
       return;
     }
     if (!is_pro) {
@@ -455,16 +468,13 @@ SubgraphPlan lower_subgraph(const ComputeDAG& dag, const FusedSubgraph& sg) {
         op.conv = ci;
         op.conv.w_tensor = wname;
         op.conv.f = dag.at(wname).shape[0];
+        reindex(op.addr);
         return;
       }
     }
-    if (s.value->kind != ExprKind::Load || dag.at(s.value->name).kind != NodeKind::Input)
+    if (!reindex(op.addr))
       fail("prologue '", s.name, "' is not a pure re-index of a graph input (arithmetic prologues are out of scope)");
-    std::map<std::string, Expr> sub_map;
-    for (size_t d = 0; d < s.axes.size(); ++d) sub_map[s.axes[d].name] = idx[d];
     op.kind = OperandPlan::Strided;
-    op.addr.tensor = s.value->name;
-    for (const auto& i : s.value->args) op.addr.idx.push_back(fold(substitute(i, sub_map)));
   };
   lower_operand(ia, sp.a);
   lower_operand(ib, sp.b);
@@ -733,9 +743,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
     if (k.bn < 16 || k.bn > 256 || k.bn % 16) fail("block_n must be 16..256 in steps of 16");
     k.stages = plan.cfg.pipeline ? plan.cfg.stages : 2;
     p.num_kb = static_cast<int32_t>((sp.K + BK - 1) / BK);
-    p.tiles_m = static_cast<int32_t>((sp.M + 127) / 128);
     p.tiles_n = static_cast<int32_t>((sp.N + k.bn - 1) / k.bn);
-    // ---- operand A
     auto strided_of = [&](const Fit& f, const tm_tensor& t) {
       Strided s{};
       s.ptr = t.data;
@@ -744,8 +752,21 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       return s;
     };
     std::string why;
+    // Operand loaders for a given CTA group (cg = 2: each CTA stages BN/2 rows of B).
+    auto bind_operands = [&](int cg) {
+    const int bn_cta = k.bn / cg;
     bool im2col_tma = false;
-    if (sp.a.kind == OperandPlan::Im2col) {
+    // conv operands whose re-index map is a plain K-major tile (1x1 stride-1
+    // conv on channels-last data) use ordinary TMA tiles instead of im2col
+    bool conv_as_gemm = false;
+    if (sp.a.kind == OperandPlan::Im2col && !sp.a.addr.idx.empty() && sp.b.kind == OperandPlan::ConvFilter &&
+        !sp.b.addr.idx.empty()) {
+      Fit fa, fb;
+      std::string w2;
+      conv_as_gemm = fit_address(sp.a.addr, *opa, sp.M, sp.K, sp.batch, fa, w2) && tma_ok_kmajor(fa, *opa, sp.M, want_dt) &&
+                     fit_address(sp.b.addr, *opb, sp.N, sp.K, sp.batch, fb, w2) && tma_ok_kmajor(fb, *opb, sp.N, want_dt);
+    }
+    if (sp.a.kind == OperandPlan::Im2col && !conv_as_gemm) {
       const ConvInfo& c = sp.a.conv;
       const tm_tensor& x = *opa;
       ConvGeom& g = p.conv;
@@ -781,7 +802,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       }
     }
     // ---- operand B
-    if (sp.b.kind == OperandPlan::ConvFilter) {
+    if (sp.b.kind == OperandPlan::ConvFilter && !conv_as_gemm) {
       const tm_tensor& w = *opb;
       ConvGeom& g = p.conv;
       g.f = static_cast<int32_t>(sp.N);
@@ -799,13 +820,13 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
         p.b_loader = LD_TMA_K;
         const uint64_t dims[3] = {(uint64_t)sp.K, (uint64_t)sp.N, 1};
         const uint64_t strides[2] = {(uint64_t)(row_stride * esize(w.dtype)), (uint64_t)(row_stride * sp.N * esize(w.dtype))};
-        const uint32_t box[3] = {(uint32_t)BK, (uint32_t)k.bn, 1u};
+        const uint32_t box[3] = {(uint32_t)BK, (uint32_t)bn_cta, 1u};
         make_tma_2d3d(k.tma_b, w.data, w.dtype, 3, dims, strides, box);
       } else {
         p.b_loader = LD_FILTER_GATHER;
       }
     } else {
-      if (sp.b.kind != OperandPlan::Strided) fail("operand B must be a strided tensor or a conv filter");
+      if (sp.b.addr.idx.empty()) fail("operand B must be a strided tensor or a conv filter");
       Fit f;
       if (!fit_address(sp.b.addr, *opb, sp.N, sp.K, sp.batch, f, why)) fail("operand B '", sp.b.addr.tensor, "': ", why);
       p.b = strided_of(f, *opb);
@@ -814,9 +835,9 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
         const uint64_t dims[3] = {(uint64_t)sp.K, (uint64_t)sp.N, (uint64_t)sp.batch};
         const uint64_t strides[2] = {(uint64_t)(f.lo * esize(opb->dtype)),
                                      (uint64_t)(std::max<int64_t>(f.c2, f.lo * sp.N) * esize(opb->dtype))};
-        const uint32_t box[3] = {(uint32_t)BK, (uint32_t)k.bn, 1u};
+        const uint32_t box[3] = {(uint32_t)BK, (uint32_t)bn_cta, 1u};
         make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * esize(opb->dtype), opb->dtype, 3, dims, strides, box);
-      } else if (!k.tf32 && k.bn % 64 == 0 && tma_ok_mnmajor(f, *opb, sp.N)) {
+      } else if (!k.tf32 && bn_cta % 64 == 0 && tma_ok_mnmajor(f, *opb, sp.N)) {
         p.b_loader = LD_TMA_MN;
         const uint64_t dims[3] = {(uint64_t)sp.N, (uint64_t)sp.K, (uint64_t)sp.batch};
         const uint64_t strides[2] = {(uint64_t)(f.c1 * 2), (uint64_t)(std::max<int64_t>(f.c2, f.c1 * sp.K) * 2)};
@@ -826,9 +847,19 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
         p.b_loader = LD_GATHER;
       }
     }
+    const bool a_tma = p.a_loader == LD_TMA_K || p.a_loader == LD_IM2COL_TMA;
+    const bool b_tma = p.b_loader == LD_TMA_K || p.b_loader == LD_TMA_MN;
+    return a_tma && b_tma;
+    };
+    // SM-pair (cta_group::2, 256-row tiles) when requested and every operand is TMA-fed
+    k.cg = 1;
+    if (plan.cfg.block_m == 256 && (k.bn == 128 || k.bn == 256) && bind_operands(2)) k.cg = 2;
+    else bind_operands(1);
+    p.tiles_m = static_cast<int32_t>((sp.M + 128 * k.cg - 1) / (128 * k.cg));
     // ---- epilogue
     if (sp.ops.size() > static_cast<size_t>(kMaxEpiOps)) fail("epilogue longer than ", kMaxEpiOps, " ops");
     p.n_ops = static_cast<int32_t>(sp.ops.size());
+    int mat_slots = 0;
     for (size_t i = 0; i < sp.ops.size(); ++i) {
       EpiOp& o = p.ops[i];
       o.kind = sp.ops[i].kind;
@@ -842,6 +873,17 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
         o.ptr = t.data;
         o.dtype = t.dtype;
         o.a = to_addr(f);
+        // where the epilogue keeps it (see SideKind)
+        if (o.a.s_col == 0) {
+          o.side = SIDE_ROW;
+        } else if (o.a.s_hi == 0 && o.a.s_lo == 0) {
+          o.side = SIDE_COL;
+        } else {
+          if (mat_slots >= kMaxMatOps) fail("epilogue has more than ", kMaxMatOps, " full-tile side operands (unsupported)");
+          o.side = SIDE_MAT;
+          o.slot = mat_slots++;
+          p.has_mat = 1;
+        }
       }
     }
     {
@@ -853,10 +895,37 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       p.out_a = to_addr(f);
     }
     if (const char* sw = std::getenv("TMB_MN_SWAP")) p.mn_lbo_sbo_swap = std::atoi(sw);
+    p.fast_math = p.out_dtype != TM_F32;  // approximate tanh only where the output rounding dominates
+    // split-K: every split gets a non-empty k-block range
+    {
+      int s = std::max(1, std::min(plan.cfg.split_k, p.num_kb));
+      p.kb_per_split = (p.num_kb + s - 1) / s;
+      p.split_k = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
+      if (p.split_k > 1) {
+        const int64_t tiles = int64_t(sp.batch) * p.tiles_m * p.tiles_n * k.cg;
+        void* ws = nullptr;
+        void* cnt = nullptr;
+        if (cudaMalloc(&ws, tiles * p.split_k * 128 * int64_t(k.bn) * 4) != cudaSuccess ||
+            cudaMalloc(&cnt, tiles * 4) != cudaSuccess || cudaMemset(cnt, 0, tiles * 4) != cudaSuccess)
+          fail("cudaMalloc failed for the split-K workspace");
+        ex->scratch.push_back(ws);
+        ex->scratch.push_back(cnt);
+        p.workspace = static_cast<float*>(ws);
+        p.counters = static_cast<int32_t*>(cnt);
+      }
+    }
     int grid = plan.cfg.grid > 0 ? std::min(plan.cfg.grid, sms * 4) : sms;
-    int used = grid;
-    p.tile_map = tile_mapping(sp.batch, p.tiles_m, p.tiles_n, grid, plan.cfg.raster, used);
-    k.grid = used;
+    int used = grid / k.cg;
+    p.tile_map = tile_mapping(int64_t(sp.batch) * p.split_k, p.tiles_m, p.tiles_n, grid / k.cg, plan.cfg.raster, used);
+    k.grid = used * k.cg;  // workers of the tile mapping are CTA pairs when cg == 2
+    if (std::getenv("TMB_TRACE")) {  // per-tile role timeline (tm_exec_trace)
+      void* tr = nullptr;
+      const size_t bytes = size_t(k.grid) * kTraceTiles * kTraceEvents * 8;
+      if (cudaMalloc(&tr, bytes) != cudaSuccess || cudaMemset(tr, 0, bytes) != cudaSuccess)
+        fail("cudaMalloc failed for the trace buffer");
+      ex->scratch.push_back(tr);
+      p.trace = static_cast<long long*>(tr);
+    }
     ex->kernels.push_back(k);
   }
   return ex;

@@ -75,7 +75,7 @@ std::unique_ptr<Plan> build_plan(const taskmap::ComputeDAG& dag, const taskmap::
 // A plan bound to tensors: fully formed kernel parameter blocks.
 struct BoundKernel {
   GemmParams p;
-  int bn = 128, stages = 4, tf32 = 0, grid = 148, simt = 0;
+  int bn = 128, stages = 4, tf32 = 0, grid = 148, simt = 0, cg = 1;
   alignas(64) unsigned char tma_a[128];
   alignas(64) unsigned char tma_b[128];
 };

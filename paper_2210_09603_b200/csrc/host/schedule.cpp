@@ -58,13 +58,27 @@ std::vector<ScheduleConfig> schedule_space(const std::string& op_kind) {
   if (op_kind != "matmul" && op_kind != "conv2d" && op_kind != "batch_matmul")
     fail("unknown op kind '", op_kind, "' for schedule_space");
   std::vector<ScheduleConfig> out;
+  // single-SM tiles (128 x N): every N, double buffer or deep ring, split-K
   for (int bn : {128, 256, 192, 64})
-    for (bool deep : {true, false})
+    for (int sk : {1, 2, 4})
+      for (bool deep : {true, false})
+        for (int raster : {0, 1}) {
+          ScheduleConfig c;
+          c.block_n = bn;
+          c.split_k = sk;
+          c.pipeline = deep;
+          c.stages = deep ? 0 : 2;
+          c.raster = raster;
+          out.push_back(c);
+        }
+  // SM-pair tiles (256 x N, tcgen05.mma.cta_group::2), deep ring
+  for (int bn : {256, 128})
+    for (int sk : {1, 2, 4})
       for (int raster : {0, 1}) {
         ScheduleConfig c;
+        c.block_m = 256;
         c.block_n = bn;
-        c.pipeline = deep;
-        c.stages = deep ? 0 : 2;
+        c.split_k = sk;
         c.raster = raster;
         out.push_back(c);
       }

@@ -86,10 +86,10 @@ void make_tma_im2col(void* map, const void* ptr, int dtype, const uint64_t* dims
 
 namespace {
 
-template <int BN, int STAGES, bool TF32>
+template <int BN, int STAGES, bool TF32, int CG>
 void launch_one(const BoundKernel& k, cudaStream_t s) {
-  using Cfg = GemmCfg<BN, STAGES, TF32>;
-  auto fn = tm_gemm_kernel<BN, STAGES, TF32>;
+  using Cfg = GemmCfg<BN, STAGES, TF32, CG>;
+  auto fn = tm_gemm_kernel<BN, STAGES, TF32, CG>;
   static bool attr_set = false;
   if (!attr_set) {
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES) != cudaSuccess)
@@ -99,11 +99,32 @@ void launch_one(const BoundKernel& k, cudaStream_t s) {
   CUtensorMap ta, tb;
   std::memcpy(&ta, k.tma_a, sizeof(ta));
   std::memcpy(&tb, k.tma_b, sizeof(tb));
-  fn<<<k.grid, kNumThreads, Cfg::SMEM_BYTES, s>>>(k.p, ta, tb);
+  if constexpr (CG == 1) {
+    fn<<<k.grid, kNumThreads, Cfg::SMEM_BYTES, s>>>(k.p, ta, tb);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(k.grid);
+    cfg.blockDim = dim3(kNumThreads);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, fn, k.p, ta, tb) != cudaSuccess)
+      taskmap::fail("cudaLaunchKernelEx (cluster) failed: ", cudaGetErrorString(cudaGetLastError()));
+  }
 }
 
-// stage counts chosen to fill ~200 KB of shared memory
-constexpr int stages_for(int bn) { return bn <= 64 ? 8 : bn <= 128 ? 6 : bn <= 192 ? 5 : 4; }
+// stage counts chosen to fill ~200 KB of shared memory (per-CTA stage bytes
+// are 16 KB of A + BN/CG rows of B)
+constexpr int stages_for(int bn, int cg) {
+  const int kb = 16 + bn / cg / 8;  // KB per stage
+  return (192 / kb) > 8 ? 8 : (192 / kb);
+}
 
 }  // namespace
 
@@ -113,21 +134,35 @@ void launch_bound(const BoundKernel& k, void* stream) {
 #define TMB_CASE(BN)                                                               \
   case BN:                                                                         \
     if (k.tf32) {                                                                  \
-      if (deep) launch_one<BN, stages_for(BN), true>(k, s);                        \
-      else launch_one<BN, 2, true>(k, s);                                          \
+      if (deep) launch_one<BN, stages_for(BN, 1), true, 1>(k, s);                  \
+      else launch_one<BN, 2, true, 1>(k, s);                                       \
     } else {                                                                       \
-      if (deep) launch_one<BN, stages_for(BN), false>(k, s);                       \
-      else launch_one<BN, 2, false>(k, s);                                         \
+      if (deep) launch_one<BN, stages_for(BN, 1), false, 1>(k, s);                 \
+      else launch_one<BN, 2, false, 1>(k, s);                                      \
     }                                                                              \
     break;
-  switch (k.bn) {
-    TMB_CASE(64)
-    TMB_CASE(128)
-    TMB_CASE(192)
-    TMB_CASE(256)
-    default: taskmap::fail("no kernel instantiated for block_n=", k.bn);
+#define TMB_CASE2(BN)                                                              \
+  case BN:                                                                         \
+    if (k.tf32) launch_one<BN, stages_for(BN, 2), true, 2>(k, s);                  \
+    else launch_one<BN, stages_for(BN, 2), false, 2>(k, s);                        \
+    break;
+  if (k.cg == 2) {
+    switch (k.bn) {
+      TMB_CASE2(128)
+      TMB_CASE2(256)
+      default: taskmap::fail("no 2-CTA kernel instantiated for block_n=", k.bn);
+    }
+  } else {
+    switch (k.bn) {
+      TMB_CASE(64)
+      TMB_CASE(128)
+      TMB_CASE(192)
+      TMB_CASE(256)
+      default: taskmap::fail("no kernel instantiated for block_n=", k.bn);
+    }
   }
 #undef TMB_CASE
+#undef TMB_CASE2
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) taskmap::fail("kernel launch failed: ", cudaGetErrorString(e));
 }

@@ -80,6 +80,8 @@ def load_library():
         "tm_exec_destroy": ([P], None),
         "tm_exec_launch": ([P, P], I32),
         "tm_exec_num_launches": ([P], I32),
+        "tm_exec_kernel_info": ([P, I32] + [ctypes.POINTER(I32)] * 6, I32),
+        "tm_exec_trace": ([P, I32, ctypes.POINTER(I64), SZ], I32),
         "tm_plan_launch": ([P, ctypes.POINTER(TmTensor), I32, ctypes.POINTER(TmTensor), I32, P], I32),
         "tm_tune": ([ctypes.c_char_p, ctypes.POINTER(TmTensor), I32, ctypes.POINTER(TmTensor), I32, I32, I32,
                      ctypes.POINTER(TmScheduleConfig), ctypes.POINTER(P)], I32),
@@ -477,6 +479,20 @@ class Exec:
     @property
     def num_launches(self) -> int:
         return load_library().tm_exec_num_launches(self._h)
+
+    def kernel_info(self, index: int = 0) -> dict:
+        v = [ctypes.c_int32() for _ in range(6)]
+        _check(load_library().tm_exec_kernel_info(self._h, index, *[ctypes.byref(x) for x in v]))
+        return dict(zip(("grid", "cta_group", "block_n", "split_k", "a_loader", "b_loader"), [x.value for x in v]))
+
+    def trace(self, index: int = 0):
+        """Per-tile role timeline (needs TMB_TRACE=1 at bind time): int64 [grid, 64, 8]."""
+        import numpy as np
+        g = self.kernel_info(index)["grid"]
+        buf = np.zeros((g, 64, 8), dtype=np.int64)
+        _check(load_library().tm_exec_trace(self._h, index, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
+                                            buf.size))
+        return buf
 
     def launch(self, stream=None):
         import torch

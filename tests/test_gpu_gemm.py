@@ -29,14 +29,15 @@ def _matmul_case(m, n, k, exact, seed):
     return a, b, bias
 
 
-@pytest.mark.parametrize("bn", [64, 128, 192, 256])
+@pytest.mark.parametrize("bm,bn", [(128, 64), (128, 128), (128, 192), (128, 256), (256, 128), (256, 256)])
 @pytest.mark.parametrize("b_layout", [None, "t"])  # B[K,N] MN-major (TMA MN) / K-major storage
-def test_matmul_bias_relu_exact(bn, b_layout):
-    m, n, k = 256, 320, 192
+def test_matmul_bias_relu_exact(bm, bn, b_layout):
+    """block_m=256 runs the SM-pair form (tcgen05.mma.cta_group::2)."""
+    m, n, k = 640, 320, 192
     a, b, bias = _matmul_case(m, n, k, True, 2)
     dag = matmul_epilogue_dag(m, n, k, DType.I32)
     got, _ = run(dag, {"A": dev(a), "B": dev(b, layout=b_layout), "Bias": dev(bias, "f32")}, {"D": (m, n)},
-                 cfg=ScheduleConfig(block_n=bn))
+                 cfg=ScheduleConfig(block_m=bm, block_n=bn))
     want = oracle_eval(dag, {"A": a, "B": b, "Bias": bias}, {"D": (m, n)}) if have_ref() else \
         {"D": port.matmul_bias_relu(a, b, bias)}
     assert np.array_equal(got["D"], want["D"])
@@ -44,14 +45,38 @@ def test_matmul_bias_relu_exact(bn, b_layout):
 
 @pytest.mark.parametrize("pipeline", [True, False])
 @pytest.mark.parametrize("raster", [0, 1])
-def test_matmul_schedule_variants_bit_identical(pipeline, raster):
-    """pipeline on/off (and any config) are bit-identical on i32 data."""
+@pytest.mark.parametrize("split_k", [1, 3])
+def test_matmul_schedule_variants_bit_identical(pipeline, raster, split_k):
+    """pipeline on/off and split-K are bit-identical on i32 data."""
     m, n, k = 384, 256, 320
     a, b, bias = _matmul_case(m, n, k, True, 7)
     dag = matmul_epilogue_dag(m, n, k, DType.I32)
     got, _ = run(dag, {"A": dev(a), "B": dev(b), "Bias": dev(bias, "f32")}, {"D": (m, n)},
-                 cfg=ScheduleConfig(pipeline=pipeline, stages=0 if pipeline else 2, raster=raster))
+                 cfg=ScheduleConfig(pipeline=pipeline, stages=0 if pipeline else 2, raster=raster, split_k=split_k))
     assert np.array_equal(got["D"], port.matmul_bias_relu(a, b, bias))
+
+
+@pytest.mark.parametrize("bm,bn,split_k", [(128, 128, 2), (256, 256, 4), (256, 128, 5), (128, 64, 8)])
+def test_split_k_repeat_launch_deterministic(bm, bn, split_k):
+    """Split-K with self-resetting tile counters: repeated launches give identical results."""
+    import torch
+    from paper_2210_09603_b200 import Plan
+    m, n, k = 520, 384, 1000
+    rng = port.Rng(31)
+    a, b = rounded(rng.tensor((m, k)), "bf16"), rounded(rng.tensor((k, n)), "bf16")
+    bias = rng.tensor((n,))
+    dag = matmul_epilogue_dag(m, n, k)
+    out = torch.empty((m, n), dtype=torch.float32, device="cuda")
+    ex = Plan(dag, ScheduleConfig(block_m=bm, block_n=bn, split_k=split_k)).bind(
+        [dev(a), dev(b), dev(bias, "f32")], [out])
+    results = []
+    for _ in range(3):
+        out.fill_(float("nan"))
+        ex.launch()
+        torch.cuda.synchronize()
+        results.append(out.cpu().numpy().copy())
+    assert all(np.array_equal(results[0], r) for r in results[1:])
+    assert port.max_rel_error(results[0], port.matmul_bias_relu(a, b, bias)) <= 1e-4
 
 
 def test_matmul_float_tolerance():
@@ -132,8 +157,8 @@ def test_batched_matmul_scale(kt_layout):
 @pytest.mark.parametrize("geom", [(2, 64, 8, 8, 64, 3, 3, 1, 1), (2, 64, 9, 9, 128, 3, 3, 2, 1),
                                   (2, 128, 7, 7, 64, 1, 1, 1, 0), (2, 64, 8, 8, 256, 1, 1, 2, 0),
                                   (1, 3, 20, 20, 64, 7, 7, 2, 3)])
-@pytest.mark.parametrize("layout", [None, "cl"])
-def test_conv_bn_relu_exact(geom, layout):
+@pytest.mark.parametrize("layout,bm", [(None, 128), ("cl", 128), ("cl", 256)])
+def test_conv_bn_relu_exact(geom, layout, bm):
     """im2col prologue + BN-fold/ReLU + NCHW re-index epilogue, exact on i32 data."""
     n, c, h, w, f, kh, kw, s, p = geom
     rng = port.Rng(4)
@@ -144,7 +169,8 @@ def test_conv_bn_relu_exact(geom, layout):
     dag = conv_bn_relu_dag(n, c, h, w, f, kh, kw, s, p, DType.I32)
     ho, wo = port.conv_out_extent(h, kh, s, p), port.conv_out_extent(w, kw, s, p)
     got, plan = run(dag, {"X": dev(x, layout=layout), "W": dev(wt, layout=layout), "Scale": dev(scale, "f32"),
-                          "Shift": dev(shift, "f32")}, {"Z": (n, f, ho, wo)})
+                          "Shift": dev(shift, "f32")}, {"Z": (n, f, ho, wo)},
+                    cfg=ScheduleConfig(block_m=bm, block_n=128 if bm == 256 else 128))
     want = port.conv_bn_relu(x, wt, scale, shift, s, p)
     assert np.array_equal(got["Z"], want)
     if have_ref() and n * f * ho * wo * c * kh * kw < 3e6:
@@ -178,9 +204,12 @@ def test_ffn_chain():
                     out_dtype="bf16")
     assert len(plan.describe()["kernels"]) == 2
     # The device stores the intermediate H in bf16 (the fp64 oracle cannot
-    # express that rounding, expr.hpp:16). With it modelled, the only error
-    # left is the bf16 output rounding: max_rel_error <= 1e-2.
-    assert port.max_rel_error(got["O"], port.ffn(x, w1, b1, w2, b2, round_h=port.round_bf16)) <= 1e-2
+    # express that rounding, expr.hpp:16) and, because H is bf16, evaluates its
+    # GELU with tanh.approx (rel. err 2^-11, below bf16's 2^-8 ulp). With the
+    # bf16 rounding modelled, the remaining error is the bf16 output rounding
+    # plus the accumulated tanh.approx error: max_rel_error <= 2e-2 (the bf16
+    # chain tolerance of SURVEY.md §8c).
+    assert port.max_rel_error(got["O"], port.ffn(x, w1, b1, w2, b2, round_h=port.round_bf16)) <= 2e-2
     # Unmodelled, the bf16(H) error (~2^-9 |H| per term, summed over dff) is an
     # absolute error, so bound it relative to the output scale.
     want = port.ffn(x, w1, b1, w2, b2)
