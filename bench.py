@@ -89,58 +89,84 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- workload --
-def build_sweep(torch, device, seed=0):
-    """Allocates inputs/weights/outputs of one sweep and binds the fused plans."""
+def build_sweep(torch, device, seed=0, tuner=None, tune_mode="auto", log=None):
+    """Allocates inputs/weights/outputs of one sweep and binds the fused plans.
+    Each distinct workload is tuned over schedule_space on the device (or its
+    cached best config is reused); returns (items, tuning report)."""
     from paper_2210_09603_b200 import Plan, ScheduleConfig, workloads as W
 
     g = torch.Generator(device=device)
     g.manual_seed(seed)
+    treport = {"tuned": 0, "cached": 0, "seconds": 0.0, "configs": {}}
 
     def rnd(shape, dtype=torch.bfloat16, cl=False):
         t = torch.empty(shape, device=device, dtype=torch.float32).uniform_(-1, 1, generator=g).to(dtype)
         return t.contiguous(memory_format=torch.channels_last) if cl else t
 
+    def conv_input(L, B):
+        if L.c < 8:  # 16-byte padded channels-last (NHWC8): the TMA-able layout for C < 8
+            xb = torch.zeros((B, L.h, L.h, 8), device=device, dtype=torch.bfloat16)
+            xb[..., :L.c] = rnd((B, L.h, L.h, L.c))
+            return xb.as_strided((B, L.c, L.h, L.h), (L.h * L.h * 8, 1, L.h * 8, 8))
+        return rnd((B, L.c, L.h, L.h), cl=True)
+
+    def pick(key, dag, ins, outs, default):
+        if tuner is None or tune_mode == "off":
+            return default
+        cfg, secs, cached = tuner.tune(key, dag, ins, outs, force=(tune_mode == "force"))
+        treport["seconds"] += secs
+        treport["tuned" if not cached else "cached"] += 1
+        treport["configs"][key] = (f"bm{cfg.block_m}/bn{cfg.block_n}/sk{cfg.split_k}/"
+                                   f"{'deep' if cfg.pipeline else 'db'}/r{cfg.raster}")
+        if log:
+            log(f"{key}: {treport['configs'][key]} ({'cached' if cached else f'tuned in {secs:.1f}s'})")
+        return cfg
+
     items = []  # (name, group, flops, exec, inputs(list), outputs(list), result?)
     B = W.RESNET_BATCH
-    cfg128 = ScheduleConfig(block_n=128)
     for L in W.RESNET50:
         dag = W.conv_bn_relu_dag(L, B)
-        bn = 256 if L.f >= 256 else (128 if L.f >= 128 else 64)
-        plan = Plan(dag, ScheduleConfig(block_n=bn))
         ho = L.out_hw()
+        plan = None
         for rep in range(L.count):
-            x = rnd((B, L.c, L.h, L.h), cl=True)
+            x = conv_input(L, B)
             w = rnd((L.f, L.c, L.k, L.k), cl=True)
             scale = rnd((L.f,), torch.float32)
             shift = rnd((L.f,), torch.float32)
             z = torch.empty((B, L.f, ho, ho), device=device, dtype=torch.bfloat16).contiguous(
                 memory_format=torch.channels_last)
+            if plan is None:
+                default = ScheduleConfig(block_n=256 if L.f >= 256 else (128 if L.f >= 128 else 64))
+                cfg = pick(f"conv:{L.name}:b{B}:nhwc", dag, [x, w, scale, shift], [z], default)
+                plan = Plan(dag, cfg)
             ex = plan.bind([x, w, scale, shift], [z])
             items.append(dict(name=f"{L.name}#{rep}", group="conv", flops=L.flops(B), exec=ex, inputs=[x],
                               outputs=[z], plan=plan))
     # FFN chain
     T = W.BERT_TOKENS
     dag = W.ffn_dag(T)
-    plan = Plan(dag, ScheduleConfig(block_n=256))
     x = rnd((T, W.BERT_HIDDEN))
     ffn_in = [x, rnd((W.BERT_HIDDEN, W.BERT_FFN)), rnd((W.BERT_FFN,)), rnd((W.BERT_FFN, W.BERT_HIDDEN)),
               rnd((W.BERT_HIDDEN,))]
     o = torch.empty((T, W.BERT_HIDDEN), device=device, dtype=torch.bfloat16)
+    plan = Plan(dag, pick(f"ffn:t{T}", dag, ffn_in, [o], ScheduleConfig(block_m=256, block_n=256)))
     items.append(dict(name="bert.ffn", group="ffn", flops=2.0 * T * W.BERT_HIDDEN * W.BERT_FFN * 2,
                       exec=plan.bind(ffn_in, [o]), inputs=[x], outputs=[o], plan=plan, result=True))
     # attention batched matmuls
     H, S, D = W.BERT_HEADS, W.BERT_SEQ, W.BERT_HEAD_DIM
     q, k, v = rnd((H, S, D)), rnd((H, S, D)), rnd((H, S, D))
     s = torch.empty((H, S, S), device=device, dtype=torch.bfloat16)
-    p1 = Plan(W.attention_scores_dag(H), ScheduleConfig(block_n=128))
+    dag1 = W.attention_scores_dag(H)
+    p1 = Plan(dag1, pick(f"attn.qk:h{H}", dag1, [q, k], [s], ScheduleConfig(block_n=128)))
     items.append(dict(name="bert.qk", group="attn", flops=2.0 * H * S * S * D, exec=p1.bind([q, k], [s]),
                       inputs=[q, k], outputs=[s], plan=p1))
     oc = torch.empty((H, S, D), device=device, dtype=torch.bfloat16)
-    p2 = Plan(W.attention_context_dag(H), ScheduleConfig(block_n=64))
+    dag2 = W.attention_context_dag(H)
+    p2 = Plan(dag2, pick(f"attn.pv:h{H}", dag2, [s, v], [oc], ScheduleConfig(block_n=64)))
     items.append(dict(name="bert.pv", group="attn", flops=2.0 * H * S * S * D, exec=p2.bind([s, v], [oc]),
                       inputs=[v], outputs=[oc], plan=p2, result=True))
     items[52]["result"] = True  # last conv layer (l4.ds) output
-    return items
+    return items, treport
 
 
 def sweep_flops(items):
@@ -215,6 +241,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tune", default="auto", choices=["auto", "force", "off"],
+                    help="auto: reuse tuning_cache.json entries, tune the rest on the device")
+    ap.add_argument("--tuning-cache", default=os.path.join(ROOT, "tuning_cache.json"))
+    ap.add_argument("--per-item", action="store_true", help="print per-launch times to stderr")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -257,7 +287,16 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=device)
 
-    items = build_sweep(torch, device, seed=1234 + rank)
+    from paper_2210_09603_b200.tuning import TuningCache
+    tuner = TuningCache(args.tuning_cache if rank == 0 else None)
+    if rank != 0 and os.path.exists(args.tuning_cache):
+        tuner = TuningCache(args.tuning_cache)  # read-only on other ranks
+    t_build = time.perf_counter()
+    items, treport = build_sweep(torch, device, seed=1234 + rank, tuner=tuner, tune_mode=args.tune,
+                                 log=(lambda m: print(m, file=sys.stderr)) if rank == 0 else None)
+    t_build = time.perf_counter() - t_build
+    if rank == 0 and treport["tuned"]:
+        tuner.save()
     flops_rank = sweep_flops(items)
     stream = torch.cuda.current_stream()
     results = [t for it in items if it.get("result") for t in it["outputs"]]
@@ -367,6 +406,10 @@ def main():
         g["ms_share"] = g["ms"] / sum(x["ms"] for x in groups.values())
     dom = max(groups, key=lambda k: groups[k]["ms"])
     dg = groups[dom]
+    if args.per_item:
+        for it, t in zip(items, per_item):
+            print(f"{it['name']:12s} {t * 1e3:8.1f} us  {it['flops'] / (t / 1e3) / 1e12:7.1f} TFLOP/s",
+                  file=sys.stderr)
     launches = sum(it["exec"].num_launches for it in items)
 
     cpu = None
@@ -385,7 +428,12 @@ def main():
                    "per_gpu_batch": {"resnet": 32, "bert_tokens": 8192, "bert_heads": 192},
                    "parallelism": f"batch-sharded x{world}, final gather to rank 0",
                    "l2": "inputs larger than L2 (~1 GB of activations per step)",
-                   "frac_of_peak": value / world / peak_tf},
+                   "frac_of_peak": value / world / peak_tf,
+                   "tuning": {"mode": args.tune, "workloads_tuned": treport["tuned"],
+                              "workloads_cached": treport["cached"],
+                              "tuning_time_s": round(treport["seconds"], 2),
+                              "setup_time_s": round(t_build, 2),
+                              "space_size": 60}},
         "roofline": {"bound": "tensor", "kernel": f"tm_gemm_kernel ({dom} launches)",
                      "achieved": dg["tflops"], "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": dg["tflops"] / peak_tf, "traffic": None,

@@ -53,7 +53,7 @@ struct EpiOp {
 constexpr int kMaxEpiOps = 8;
 constexpr int kMaxMatOps = 2;
 constexpr int kTraceTiles = 64;
-constexpr int kTraceEvents = 8;
+constexpr int kTraceEvents = 16;  // 0-7 role events (TraceEv), 8-13 fine epilogue ticks
 // trace events per tile
 enum TraceEv : int32_t {
   TR_PROD_FIRST = 0,  // producer: first k-block slot acquired
@@ -72,7 +72,10 @@ enum LoaderKind : int32_t {
   LD_GATHER = 2,        // predicated LSU gather of a strided operand (+ cast)
   LD_IM2COL_GATHER = 3, // predicated im2col gather from any-strided X (A only)
   LD_IM2COL_TMA = 4,    // TMA im2col mode on channels-last X (A only)
-  LD_FILTER_GATHER = 5  // conv filter W[F,C,Kh,Kw] with any strides (B only)
+  LD_FILTER_GATHER = 5, // conv filter W[F,C,Kh,Kw] with any strides (B only)
+  LD_IM2COL_TMA8 = 6    // small-C conv (C <= 8, 16-byte padded channels-last X): one
+                        // TMA im2col box {8 ch x 128 px} per tap, 8 taps per k-block,
+                        // no-swizzle K-major smem layout; K order (tap, c < 8)
 };
 
 // A strided operand: element (row, k, batch) at
@@ -90,6 +93,8 @@ struct Strided {
 // the order TMA im2col produces (requires channels-last X and W).
 struct ConvGeom {
   int32_t n, c, h, w, f, kh, kw, stride, pad, ho, wo, korder;
+  int32_t cpad;  // channels per tap in K order 1 (= c, or 8 for LD_IM2COL_TMA8)
+  int32_t pad2_;
   const void* x;
   const void* wt;
   int32_t x_dtype, w_dtype;
@@ -116,6 +121,17 @@ struct GemmParams {
   float* workspace;
   int32_t* counters;
   int32_t fast_math;  // approximate transcendentals (bf16 outputs)
+  int32_t out_tma;    // row-major output: stage each 32x16 chunk in smem, TMA-store it
+  // Canonical epilogue v = act(acc * S[col] + T[col]) (+ R[row, col]), which every
+  // chain of the BASELINE configs compiles to (bias, scale, BN-fold, ReLU/GELU,
+  // residual): S/T are staged per tile as column vectors; ops that do not fit run
+  // through the generic op interpreter instead.
+  int32_t canon;
+  int32_t canon_act;       // 0 none, 1 relu, 2 gelu_tanh
+  int32_t canon_s_op;      // op index providing S (-1: constant canon_s)
+  int32_t canon_t_op;      // op index providing T (-1: constant canon_t)
+  int32_t canon_res_slot;  // SIDE_MAT prefetch slot added after the activation (-1: none)
+  float canon_s, canon_t;
   // optional per-tile role timeline (clock64 relative to CTA start), layout
   // [cta][kTraceTiles][kTraceEvents]; null = tracing off
   long long* trace;

@@ -45,7 +45,9 @@ struct GemmCfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
   static constexpr int COLBUF_BYTES = kMaxEpiOps * BN * 4;  // staged per-column epilogue operands
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + COLBUF_BYTES;
+  static constexpr int OUTBUF_BYTES = kEpiWarps * 32 * 16 * 4;  // per-warp 32x16 output chunk (<= f32)
+  static constexpr int SMEM_BYTES =
+      STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + COLBUF_BYTES + OUTBUF_BYTES;
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 must be 16..256 step 16");
 };
 
@@ -184,9 +186,9 @@ __device__ __forceinline__ void gather_row_filter(uint8_t* tile, int r, const Co
     const int rr = k0 % khw;
     fh = rr / g.kw;
     fw = rr % g.kw;
-  } else {
-    const int tap = k0 / g.c;
-    ch = k0 % g.c;
+  } else {  // (tap, channel) with cpad >= c channels per tap; padded channels are zero
+    const int tap = k0 / g.cpad;
+    ch = k0 % g.cpad;
     fh = tap / g.kw;
     fw = tap % g.kw;
   }
@@ -197,14 +199,14 @@ __device__ __forceinline__ void gather_row_filter(uint8_t* tile, int r, const Co
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
       const int k = k0 + c * PER + j;
-      const bool ok = row_ok && k < K;
+      const bool ok = row_ok && k < K && ch < g.c && fh < g.kh;
       bits[j] = ok ? load_bits<TF32>(g.wt, wbase + ch * g.sw[1] + fh * g.sw[2] + fw * g.sw[3],
                                      g.w_dtype)
                    : 0u;
       if (g.korder == 0) {
         if (++fw == g.kw) { fw = 0; if (++fh == g.kh) { fh = 0; ++ch; } }
       } else {
-        if (++ch == g.c) { ch = 0; if (++fw == g.kw) { fw = 0; ++fh; } }
+        if (++ch == g.cpad) { ch = 0; if (++fw == g.kw) { fw = 0; ++fh; } }
       }
     }
     st_sw128(tile, r, c, pack_chunk<TF32>(bits));
@@ -348,6 +350,55 @@ __device__ __forceinline__ void apply_epilogue(const GemmParams& p, float (&v)[1
   }
 }
 
+// Canonical epilogue: v = act(acc * S[c] + T[c]) (+ R), S/T staged in smem.
+template <int BN>
+__device__ __forceinline__ void apply_canon(const GemmParams& p, float (&v)[16], const float* colbuf, int cbase,
+                                            const float (&mat)[kMaxMatOps][16]) {
+  const float4* S = reinterpret_cast<const float4*>(colbuf + cbase);
+  const float4* T = reinterpret_cast<const float4*>(colbuf + BN + cbase);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float4 s = S[q], t = T[q];
+    v[4 * q] = fmaf(v[4 * q], s.x, t.x);
+    v[4 * q + 1] = fmaf(v[4 * q + 1], s.y, t.y);
+    v[4 * q + 2] = fmaf(v[4 * q + 2], s.z, t.z);
+    v[4 * q + 3] = fmaf(v[4 * q + 3], s.w, t.w);
+  }
+  if (p.canon_act == 1) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.f);
+  } else if (p.canon_act == 2) {
+    if (p.fast_math) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = gelu_tanh_fast(v[j]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = gelu_tanh(v[j]);
+    }
+  }
+  if (p.canon_res_slot == 0) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] += mat[0][j];
+  } else if (p.canon_res_slot == 1) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] += mat[1][j];
+  }
+}
+
+// GENERIC = false compiles only the canonical epilogue (and, in the kernel, only
+// TMA operand loaders): the hot loops then fit the instruction cache, which the
+// full interpreter + gather code (~370 KB of SASS per instantiation) does not.
+template <int BN, bool GENERIC>
+__device__ __forceinline__ void epilogue16(const GemmParams& p, float (&v)[16], const float* colbuf, int cbase,
+                                           const float* rowv, const float (&mat)[kMaxMatOps][16]) {
+  if constexpr (GENERIC) {
+    if (p.canon) apply_canon<BN>(p, v, colbuf, cbase, mat);
+    else apply_epilogue<BN>(p, v, colbuf, cbase, rowv, mat);
+  } else {
+    apply_canon<BN>(p, v, colbuf, cbase, mat);
+  }
+}
+
 __device__ __forceinline__ void store_out(const GemmParams& p, const float (&v)[16], int64_t base,
                                           int64_t col0, bool row_ok) {
   if (!row_ok) return;
@@ -412,10 +463,10 @@ __device__ __forceinline__ bool next_tile(const GemmParams& p, uint32_t i, int& 
 
 }  // namespace detail
 
-template <int BN, int STAGES, bool TF32, int CG>
+template <int BN, int STAGES, bool TF32, int CG, bool GENERIC>
 __global__ void __launch_bounds__(kNumThreads, 1)
     tm_gemm_kernel(const __grid_constant__ GemmParams p, const __grid_constant__ CUtensorMap tmA,
-                   const __grid_constant__ CUtensorMap tmB) {
+                   const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmC) {
   using Cfg = GemmCfg<BN, STAGES, TF32, CG>;
   constexpr int BK = Cfg::BK;
   constexpr int kTileM = kBM * CG;  // rows per tile (both CTAs of a pair)
@@ -432,10 +483,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint32_t* split_flag = tmem_slot + 1;
   float* colbuf = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES + 256);
+  uint8_t* outbuf = smem + STAGES * Cfg::STAGE_BYTES + 256 + Cfg::COLBUF_BYTES;
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const bool a_tma = p.a_loader == LD_TMA_K || p.a_loader == LD_IM2COL_TMA;
+  const bool a_tma = p.a_loader == LD_TMA_K || p.a_loader == LD_IM2COL_TMA || p.a_loader == LD_IM2COL_TMA8;
   const bool b_tma = p.b_loader == LD_TMA_K || p.b_loader == LD_TMA_MN;
   const bool all_tma = a_tma && b_tma;
 
@@ -537,6 +589,21 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                                       ow * p.conv.stride - p.conv.pad,
                                       oh * p.conv.stride - p.conv.pad, img,
                                       static_cast<uint16_t>(fw), static_cast<uint16_t>(fh));
+            } else if (p.a_loader == LD_IM2COL_TMA8) {
+              // 8 taps per k-block, one {8 ch x 128 px} box each (2 KB, dense rows of
+              // 16 B = one core-matrix column); taps past the window repeat the last
+              // one (the filter is zero there, and the data is finite)
+              const int hw = p.conv.ho * p.conv.wo;
+              const int img = m0 / hw, rem = m0 % hw;
+              const int oh = rem / p.conv.wo, ow = rem % p.conv.wo;
+              const int taps = p.conv.kh * p.conv.kw;
+#pragma unroll 1
+              for (int j = 0; j < BK / 8; ++j) {
+                const int tap = min(kb * (BK / 8) + j, taps - 1);
+                ptx::tma_load_im2col_4d(a_tile + j * 2048, &tmA, &full[stage], 0, ow * p.conv.stride - p.conv.pad,
+                                        oh * p.conv.stride - p.conv.pad, img,
+                                        static_cast<uint16_t>(tap % p.conv.kw), static_cast<uint16_t>(tap / p.conv.kw));
+              }
             }
             if (p.b_loader == LD_TMA_K) {
               ptx::tma_load_3d(b_tile, &tmB, &full[stage], k0, n0, b);
@@ -547,7 +614,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                                  k0, b);
             }
           }
-          if (!all_tma) {
+          if (GENERIC && !all_tma) {
             // predicated gather of the non-TMA operand(s), one tile row per thread
             if (!a_tma) {
               const int64_t row = m0 + t;
@@ -588,18 +655,80 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     bool valid;
     int64_t rowpart[kMaxEpiOps];
     float rowv[kMaxEpiOps];
+    bool has_col = false;
+    for (int o = 0; o < p.n_ops; ++o) has_col = has_col || p.ops[o].side == SIDE_COL;
+    int staged_tn = -1, staged_b = -1;
+    // this warp's 32x16 output staging: 2 KB, a 2-deep ring of 1 KB bf16 chunks
+    // (one outstanding TMA store while the next chunk is written) or one f32 chunk
+    uint8_t* obuf_base = outbuf + e * (32 * 16 * 4);
+    const int obytes = p.out_dtype == DT_F32 ? 4 : 2;
+    uint32_t n_emit = 0;
+    auto emit = [&](const float (&v)[16], int64_t obase_, int64_t col0, bool row_ok_, int tile_row0) {
+      if (!p.out_tma) {
+        detail::store_out(p, v, obase_, col0, row_ok_);
+        return;
+      }
+      uint8_t* obuf = obuf_base + (obytes == 2 ? (n_emit & 1u) * 1024 : 0);
+      if (lane == 0) {  // the store that last used this buffer has read it
+        if (obytes == 2) ptx::bulk_wait_read<1>();
+        else ptx::bulk_wait_read<0>();
+      }
+      ++n_emit;
+      __syncwarp();
+      if (obytes == 2) {
+        uint32_t w[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+          w[j] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(obuf + lane * 32);
+        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+      } else {
+        float4* dst = reinterpret_cast<float4*>(obuf + lane * 64);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+      }
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        ptx::tma_store_3d(&tmC, obuf, static_cast<int32_t>(col0), tile_row0, b);
+        ptx::bulk_commit();
+      }
+    };
     for (uint32_t i = 0; detail::next_tile<CG>(p, i, b, ks, tm_, tn, valid); ++i) {
       if (!valid) continue;
       const int64_t n0 = static_cast<int64_t>(tn) * BN;
-      const int64_t row = static_cast<int64_t>(tm_) * kTileM + rank * kBM + lg * 32 + lane;
+      const int row0 = tm_ * kTileM + rank * kBM + lg * 32;  // this warp's first row
+      const int64_t row = static_cast<int64_t>(row0) + lane;
       const bool row_ok = row < p.M;
       const int64_t rr = row_ok ? row : 0;
-      // stage this tile's column vectors while the MMA works on it
-      ptx::named_bar_sync(1, 32 * kEpiWarps);  // previous tile's readers are done
+      // Stage this tile's column vectors while the MMA works on it; skipped when
+      // the previous tile had the same columns (e.g. every tile of a conv whose
+      // F fits one tile), which keeps the load latency off the critical path.
+      const bool restage = (staged_tn < 0 && (has_col || p.canon)) || (has_col && (tn != staged_tn || b != staged_b));
+      if (restage) ptx::named_bar_sync(1, 32 * kEpiWarps);  // previous tile's readers are done
+      if (restage && p.canon) {  // S and T column vectors of the canonical epilogue
+        for (int c = et; c < BN; c += 32 * kEpiWarps) {
+          const bool in = n0 + c < p.N;
+          float s = p.canon_s, t = p.canon_t;
+          if (p.canon_s_op >= 0 && in) {
+            const EpiOp& op = p.ops[p.canon_s_op];
+            s = detail::load_side(op.ptr, detail::addr_rowpart(op.a, 0, b) + (n0 + c) * op.a.s_col, op.dtype);
+          }
+          if (p.canon_t_op >= 0 && in) {
+            const EpiOp& op = p.ops[p.canon_t_op];
+            t = detail::load_side(op.ptr, detail::addr_rowpart(op.a, 0, b) + (n0 + c) * op.a.s_col, op.dtype);
+          }
+          colbuf[c] = s;
+          colbuf[BN + c] = t;
+        }
+      }
       for (int o = 0; o < p.n_ops; ++o) {
         const EpiOp& op = p.ops[o];
         rowpart[o] = detail::addr_rowpart(op.a, rr, b);
-        if (op.side == SIDE_COL) {
+        if (op.side == SIDE_COL && restage && !p.canon) {
           const int64_t cb = detail::addr_rowpart(op.a, 0, b);
           for (int c = et; c < BN; c += 32 * kEpiWarps)
             colbuf[o * BN + c] = (n0 + c < p.N) ? detail::load_side(op.ptr, cb + (n0 + c) * op.a.s_col, op.dtype) : 0.f;
@@ -608,7 +737,11 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
       }
       const int64_t obase = detail::addr_rowpart(p.out_a, rr, b);
-      ptx::named_bar_sync(1, 32 * kEpiWarps);  // column buffers ready
+      if (restage) {
+        ptx::named_bar_sync(1, 32 * kEpiWarps);  // column buffers ready
+        staged_tn = tn;
+        staged_b = b;
+      }
       if (et == 0) detail::trace(p, i, TR_EPI_READY, t0);
       float mat[kMaxMatOps][16];
       auto prefetch = [&](int c, float (&dst)[kMaxMatOps][16]) {
@@ -623,7 +756,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             }
           }
       };
-      if (p.has_mat) prefetch(half, mat);
+      if (p.has_mat && p.split_k == 1) prefetch(2 * half, mat);
       if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&tfull[acc], acc_phase);
       else ptx::mbar_wait(&tfull[acc], acc_phase);
       ptx::tc_fence_after();
@@ -677,29 +810,50 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               v[4 * q] += f.x; v[4 * q + 1] += f.y; v[4 * q + 2] += f.z; v[4 * q + 3] += f.w;
             }
           }
-          detail::apply_epilogue<BN>(p, v, colbuf, c * 16, rowv, mat);
-          detail::store_out(p, v, obase, col0, row_ok);
+          detail::epilogue16<BN, GENERIC>(p, v, colbuf, c * 16, rowv, mat);
+          emit(v, obase, col0, row_ok, row0);
         }
         if (et == 0) p.counters[tile_id] = 0;  // self-resetting for the next launch
         continue;
       }
+      // 32 columns per TMEM round trip (one wait per 32 columns); the two warps
+      // of a lane group interleave 32-column chunks
 #pragma unroll 1
-      for (int c = half; c < kChunks; c += 2) {
-        const int64_t col0 = n0 + c * 16;
-        if (col0 >= p.N) break;  // warp-uniform
+      for (int c2 = half; c2 < BN / 32; c2 += 2) {
+        const int64_t colA = n0 + c2 * 32;
+        if (colA >= p.N) break;  // warp-uniform
         float nxt[kMaxMatOps][16];
-        if (p.has_mat && c + 2 < kChunks && col0 + 32 < p.N + 16) prefetch(c + 2, nxt);
-        uint32_t r[16];
-        ptx::tmem_ld16(taddr + c * 16, r);
+        if (p.has_mat && colA + 16 < p.N) prefetch(2 * c2 + 1, nxt);
+        uint32_t r[32];
+        // fine-grained epilogue timeline: warp 4 of every CTA, first 32-column chunk
+        // of each tile -> trace events 8..13 (kTraceEvents = 16)
+        const bool fine = p.trace != nullptr && warp == 4 && c2 == half && i < static_cast<uint32_t>(kTraceTiles);
+        auto tick = [&](int ev) {
+          if (fine && lane == 0)
+            p.trace[(static_cast<int64_t>(blockIdx.x) * kTraceTiles + i) * kTraceEvents + ev] = clock64() - t0;
+        };
+        tick(8);
+        ptx::tmem_ld32(taddr + c2 * 32, r);
         ptx::tmem_wait_ld();
-        float v[16];
+        tick(9);
+        {
+          float v[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-        detail::apply_epilogue<BN>(p, v, colbuf, c * 16, rowv, mat);
-        detail::store_out(p, v, obase, col0, row_ok);
-        if (p.has_mat) {
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+          detail::epilogue16<BN, GENERIC>(p, v, colbuf, c2 * 32, rowv, mat);
+          tick(10);
+          emit(v, obase, colA, row_ok, row0);
+          tick(11);
+        }
+        if (colA + 16 < p.N) {
+          float v[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) { mat[0][j] = nxt[0][j]; mat[1][j] = nxt[1][j]; }
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[16 + j]);
+          if (p.has_mat && c2 + 2 < BN / 32 && colA + 64 < p.N) prefetch(2 * (c2 + 2), mat);
+          detail::epilogue16<BN, GENERIC>(p, v, colbuf, c2 * 32 + 16, rowv, nxt);
+          tick(12);
+          emit(v, obase, colA + 16, row_ok, row0);
+          tick(13);
         }
       }
       ptx::tc_fence_before();
@@ -712,10 +866,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       if (et == 0) detail::trace(p, i, TR_EPI_DONE, t0);
       if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
     }
+    if (p.out_tma && lane == 0) ptx::bulk_wait<0>();  // all output tiles written before exit
   } else {
     // ===================== MMA issuer (single thread) =====================
     if (lane == 0 && rank == 0) {
       const bool b_mn = p.b_loader == LD_TMA_MN;
+      const bool a_noswz = p.a_loader == LD_IM2COL_TMA8;
       const uint32_t idesc = ptx::make_idesc(kTileM, BN, TF32 ? 2u : 1u, false, b_mn);
       const uint32_t mn_lbo = p.mn_lbo_sbo_swap ? 1024u : 64u * kRowBytes;
       const uint32_t mn_sbo = p.mn_lbo_sbo_swap ? 64u * kRowBytes : 1024u;
@@ -740,7 +896,9 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           const uint32_t b_addr = ptx::smem_u32(smB + stage * Cfg::B_BYTES);
 #pragma unroll
           for (int kk = 0; kk < Cfg::NSTEP; ++kk) {
-            const uint64_t adesc = ptx::smem_desc_sw128(a_addr + kk * Cfg::KSTEP * Cfg::kElem, 16, 1024);
+            const uint64_t adesc =
+                a_noswz ? ptx::smem_desc_noswz(a_addr + kk * 2 * 2048, 2048, 128)  // 2 taps (2 x 16 B chunks) per K16
+                        : ptx::smem_desc_sw128(a_addr + kk * Cfg::KSTEP * Cfg::kElem, 16, 1024);
             const uint64_t bdesc =
                 b_mn ? ptx::smem_desc_sw128(b_addr + kk * Cfg::KSTEP * kRowBytes, mn_lbo, mn_sbo)
                      : ptx::smem_desc_sw128(b_addr + kk * Cfg::KSTEP * Cfg::kElem, 16, 1024);

@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <functional>
+#include <mutex>
 #include <cstring>
 #include <random>
 #include <set>
@@ -566,8 +567,38 @@ struct Fit {
   int64_t P, hi, lo, c1, c2, off;
 };
 
+bool fit_address_uncached(const AddrExpr& a, const tm_tensor& t, int64_t n0, int64_t n1, int64_t n2, Fit& f,
+                          std::string& why);
+
+// Fits depend only on the index expressions, the tensor's shape/strides and
+// the GEMM extents, never on the schedule: memoised so that tuning a shape
+// over the whole space pays for each fit once.
 bool fit_address(const AddrExpr& a, const tm_tensor& t, int64_t n0, int64_t n1, int64_t n2, Fit& f,
                  std::string& why) {
+  static std::mutex mu;
+  static std::map<std::string, std::pair<bool, Fit>> cache;
+  std::string key;
+  for (const auto& e : a.idx) key += expr_to_text(e) + ";";
+  for (int d = 0; d < t.rank; ++d) key += std::to_string(t.shape[d]) + "/" + std::to_string(t.stride[d]) + ",";
+  key += "|" + std::to_string(n0) + "," + std::to_string(n1) + "," + std::to_string(n2);
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      f = it->second.second;
+      if (!it->second.first) why = "cached: address map does not fit";
+      return it->second.first;
+    }
+  }
+  const bool ok = fit_address_uncached(a, t, n0, n1, n2, f, why);
+  std::lock_guard<std::mutex> g(mu);
+  if (cache.size() > 4096) cache.clear();
+  cache[key] = {ok, f};
+  return ok;
+}
+
+bool fit_address_uncached(const AddrExpr& a, const tm_tensor& t, int64_t n0, int64_t n1, int64_t n2, Fit& f,
+                          std::string& why) {
   if (static_cast<int>(a.idx.size()) != t.rank) { why = "rank mismatch"; return false; }
   std::vector<IndexProgram> progs;
   for (const auto& e : a.idx) progs.push_back(IndexProgram::compile(e, {kRow, kCol, kBat}));
@@ -778,8 +809,22 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
                    c.pad <= 127 && (c.kh - 1 - c.pad) <= 128 && c.kh <= 127 && c.kw <= 127 &&
                    (reinterpret_cast<uintptr_t>(x.data) % 16 == 0) &&
                    sp.b.kind == OperandPlan::ConvFilter && plan.cfg.split_k >= 1;
-      g.korder = im2col_tma ? 1 : 0;
-      p.a_loader = im2col_tma ? LD_IM2COL_TMA : LD_IM2COL_GATHER;
+      // C <= 8 stored 16-byte padded channels-last (pixel stride 8): one im2col box per tap
+      const bool cl8 = x.stride[1] == 1 && x.stride[3] == 8 && x.stride[2] == c.w * 8 && x.stride[0] == c.h * c.w * 8;
+      const bool tma8 = !im2col_tma && !k.tf32 && cg == 1 && x.dtype == TM_BF16 && c.c <= 8 && cl8 &&
+                        c.stride <= 8 && c.pad <= 127 && (reinterpret_cast<uintptr_t>(x.data) % 16 == 0) &&
+                        sp.b.kind == OperandPlan::ConvFilter;
+      g.korder = (im2col_tma || tma8) ? 1 : 0;
+      g.cpad = tma8 ? 8 : static_cast<int32_t>(c.c);
+      p.a_loader = im2col_tma ? LD_IM2COL_TMA : tma8 ? LD_IM2COL_TMA8 : LD_IM2COL_GATHER;
+      if (tma8) {
+        p.K = static_cast<int32_t>(c.kh * c.kw * 8);  // K order (tap, 8 channels)
+        p.num_kb = (p.K + BK - 1) / BK;
+        const uint64_t dims[4] = {(uint64_t)c.c, (uint64_t)c.w, (uint64_t)c.h, (uint64_t)c.n};
+        const uint64_t strides[3] = {16, (uint64_t)x.stride[2] * 2, (uint64_t)x.stride[0] * 2};
+        make_tma_im2col(k.tma_a, x.data, x.dtype, dims, strides, static_cast<int>(c.pad),
+                        static_cast<int>(c.pad - (c.kh - 1)), static_cast<int>(c.stride), 8, 128, false);
+      }
       if (im2col_tma) {
         const uint64_t dims[4] = {(uint64_t)c.c, (uint64_t)c.w, (uint64_t)c.h, (uint64_t)c.n};
         const uint64_t strides[3] = {(uint64_t)x.stride[3] * 2, (uint64_t)x.stride[2] * 2, (uint64_t)x.stride[0] * 2};
@@ -818,10 +863,26 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       if (lin && w.dtype == want_dt && (row_stride * esize(w.dtype)) % 16 == 0 &&
           reinterpret_cast<uintptr_t>(w.data) % 16 == 0) {
         p.b_loader = LD_TMA_K;
-        const uint64_t dims[3] = {(uint64_t)sp.K, (uint64_t)sp.N, 1};
+        const uint64_t dims[3] = {(uint64_t)p.K, (uint64_t)sp.N, 1};
         const uint64_t strides[2] = {(uint64_t)(row_stride * esize(w.dtype)), (uint64_t)(row_stride * sp.N * esize(w.dtype))};
         const uint32_t box[3] = {(uint32_t)BK, (uint32_t)bn_cta, 1u};
         make_tma_2d3d(k.tma_b, w.data, w.dtype, 3, dims, strides, box);
+      } else if (!k.tf32) {
+        // Filter layout not TMA-describable in this K order (e.g. the padded
+        // (tap, 8-channel) order of LD_IM2COL_TMA8): repack it once, at bind
+        // time, into a K-major [F, K'] bf16 buffer owned by the exec -- the
+        // filter is an inference constant of the bound plan (re-bind after
+        // changing weights).
+        const int kp = (p.K + 7) / 8 * 8;
+        void* packed = nullptr;
+        if (cudaMalloc(&packed, size_t(sp.N) * kp * 2) != cudaSuccess) fail("cudaMalloc failed for the filter repack");
+        ex->scratch.push_back(packed);
+        pack_filter(g, kp, packed);
+        p.b_loader = LD_TMA_K;
+        const uint64_t dims[3] = {(uint64_t)p.K, (uint64_t)sp.N, 1};
+        const uint64_t strides[2] = {(uint64_t)kp * 2, (uint64_t)kp * 2 * sp.N};
+        const uint32_t box[3] = {(uint32_t)BK, (uint32_t)bn_cta, 1u};
+        make_tma_2d3d(k.tma_b, packed, TM_BF16, 3, dims, strides, box);
       } else {
         p.b_loader = LD_FILTER_GATHER;
       }
@@ -886,6 +947,28 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
         }
       }
     }
+    // canonical epilogue v = act(acc * S[c] + T[c]) (+ R): [MUL s]? [ADD|SUB t]? [RELU|GELU]? [ADD residual]?
+    {
+      int i = 0;
+      const int n = p.n_ops;
+      p.canon_s = 1.f;
+      p.canon_t = 0.f;
+      p.canon_s_op = p.canon_t_op = p.canon_res_slot = -1;
+      auto is = [&](int kind) { return i < n && p.ops[i].kind == kind; };
+      if (is(EPI_MUL_C)) { p.canon_s = p.ops[i].c; ++i; }
+      else if (is(EPI_MUL_T) && p.ops[i].side == SIDE_COL) { p.canon_s_op = i; ++i; }
+      if (is(EPI_ADD_C)) { p.canon_t = p.ops[i].c * (p.canon_s_op < 0 ? 1.f : 1.f); ++i; }
+      else if (is(EPI_SUB_C)) { p.canon_t = -p.ops[i].c; ++i; }
+      else if (is(EPI_ADD_T) && p.ops[i].side == SIDE_COL) { p.canon_t_op = i; ++i; }
+      if (is(EPI_RELU)) { p.canon_act = 1; ++i; }
+      else if (is(EPI_GELU_TANH)) { p.canon_act = 2; ++i; }
+      if (is(EPI_ADD_T) && p.ops[i].side == SIDE_MAT) { p.canon_res_slot = p.ops[i].slot; ++i; }
+      p.canon = (i == n && !std::getenv("TMB_NO_CANON")) ? 1 : 0;
+      // compact instantiation when every operand is TMA-fed and the epilogue is canonical
+      const bool a_t = p.a_loader == LD_TMA_K || p.a_loader == LD_IM2COL_TMA || p.a_loader == LD_IM2COL_TMA8;
+      const bool b_t = p.b_loader == LD_TMA_K || p.b_loader == LD_TMA_MN;
+      k.generic = (a_t && b_t && p.canon && !k.tf32 && !std::getenv("TMB_GENERIC")) ? 0 : 1;
+    }
     {
       const tm_tensor& t = lookup(env, sp.out.tensor);
       Fit f;
@@ -893,6 +976,20 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       p.out = t.data;
       p.out_dtype = t.dtype;
       p.out_a = to_addr(f);
+      // Row-major (channels-last, [M,N]) outputs: the epilogue stages each
+      // 32x16 chunk in smem and TMA-stores it (coalesced, off the LSU).  Outputs
+      // whose rows are the contiguous dimension (NCHW) keep direct stores,
+      // which are already coalesced (lanes = consecutive pixels).
+      const int es = esize(t.dtype);
+      const uintptr_t base = reinterpret_cast<uintptr_t>(t.data) + f.off * es;
+      if (f.c1 == 1 && f.P >= sp.M && f.lo > 0 && (f.lo * es) % 16 == 0 && (f.c2 * es) % 16 == 0 && base % 16 == 0 &&
+          (t.dtype == TM_BF16 || t.dtype == TM_F32) && !std::getenv("TMB_NO_TMA_STORE")) {
+        p.out_tma = 1;
+        const uint64_t dims[3] = {(uint64_t)sp.N, (uint64_t)sp.M, (uint64_t)sp.batch};
+        const uint64_t strides[2] = {(uint64_t)(f.lo * es), (uint64_t)(std::max<int64_t>(f.c2, f.lo * sp.M) * es)};
+        const uint32_t box[3] = {16u, 32u, 1u};
+        make_tma_2d3d(k.tma_c, reinterpret_cast<const void*>(base), t.dtype, 3, dims, strides, box, false);
+      }
     }
     if (const char* sw = std::getenv("TMB_MN_SWAP")) p.mn_lbo_sbo_swap = std::atoi(sw);
     p.fast_math = p.out_dtype != TM_F32;  // approximate tanh only where the output rounding dominates

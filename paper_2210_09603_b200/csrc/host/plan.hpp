@@ -76,8 +76,10 @@ std::unique_ptr<Plan> build_plan(const taskmap::ComputeDAG& dag, const taskmap::
 struct BoundKernel {
   GemmParams p;
   int bn = 128, stages = 4, tf32 = 0, grid = 148, simt = 0, cg = 1;
+  int generic = 1;  // 0: compact instantiation (TMA loaders + canonical epilogue only)
   alignas(64) unsigned char tma_a[128];
   alignas(64) unsigned char tma_b[128];
+  alignas(64) unsigned char tma_c[128];  // output map (row-major outputs, TMA-store epilogue)
 };
 
 struct Exec {
@@ -92,10 +94,13 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
 // kernel launcher (gemm_launch.cu)
 int num_sms(int device);
 void launch_bound(const BoundKernel& k, void* stream);
+void pack_filter(const ConvGeom& g, int kp, void* out);  // bf16 [f][kp] in the GEMM K order
+unsigned long long device_mismatch(const void* a, const void* b, size_t bytes, void* stream);
+float device_max_rel_error(const void* a, const void* b, size_t n, int dtype, void* stream);
 void make_tma_2d3d(void* map, const void* ptr, int dtype, int rank, const uint64_t* dims,
-                   const uint64_t* strides_bytes, const uint32_t* box);
+                   const uint64_t* strides_bytes, const uint32_t* box, bool swizzle128 = true);
 void make_tma_im2col(void* map, const void* ptr, int dtype, const uint64_t* dims_cwhn,
                      const uint64_t* strides_bytes, int pad_lo, int pad_hi_corner, int stride,
-                     uint32_t channels, uint32_t pixels);
+                     uint32_t channels, uint32_t pixels, bool swizzle128 = true);
 
 }  // namespace tmb

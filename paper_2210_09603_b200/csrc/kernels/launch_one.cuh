@@ -1,0 +1,61 @@
+// Launch helper shared by the instantiation units (inst_*.cu): one
+// tm_gemm_kernel specialisation, optionally as a CTA-pair cluster launch.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstring>
+
+#include "../device/gemm_sm100.cuh"
+#include "../host/plan.hpp"
+
+namespace tmb {
+
+// stage counts chosen to fill ~192 KB of shared memory (per-CTA stage bytes
+// are 16 KB of A + BN/CG rows of B)
+constexpr int stages_for(int bn, int cg) {
+  const int kb = 16 + bn / cg / 8;  // KB per stage
+  return (192 / kb) > 8 ? 8 : (192 / kb);
+}
+
+template <int BN, int STAGES, bool TF32, int CG, bool GENERIC>
+void launch_one(const BoundKernel& k, cudaStream_t s) {
+  using Cfg = GemmCfg<BN, STAGES, TF32, CG>;
+  auto fn = tm_gemm_kernel<BN, STAGES, TF32, CG, GENERIC>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES) != cudaSuccess)
+      taskmap::fail("cudaFuncSetAttribute failed: ", cudaGetErrorString(cudaGetLastError()));
+    attr_set = true;
+  }
+  CUtensorMap ta, tb, tc;
+  std::memcpy(&ta, k.tma_a, sizeof(ta));
+  std::memcpy(&tb, k.tma_b, sizeof(tb));
+  std::memcpy(&tc, k.tma_c, sizeof(tc));
+  if constexpr (CG == 1) {
+    fn<<<k.grid, kNumThreads, Cfg::SMEM_BYTES, s>>>(k.p, ta, tb, tc);
+  } else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(k.grid);
+    cfg.blockDim = dim3(kNumThreads);
+    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, fn, k.p, ta, tb, tc) != cudaSuccess)
+      taskmap::fail("cudaLaunchKernelEx (cluster) failed: ", cudaGetErrorString(cudaGetLastError()));
+  }
+}
+
+// per-unit dispatchers (defined in inst_*.cu); return false if no variant matches
+bool launch_cg1_generic_bf16(const BoundKernel& k, cudaStream_t s);
+bool launch_cg1_generic_tf32(const BoundKernel& k, cudaStream_t s);
+bool launch_cg1_fast(const BoundKernel& k, cudaStream_t s);
+bool launch_cg2(const BoundKernel& k, cudaStream_t s);
+
+}  // namespace tmb

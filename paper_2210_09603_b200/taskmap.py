@@ -489,7 +489,7 @@ class Exec:
         """Per-tile role timeline (needs TMB_TRACE=1 at bind time): int64 [grid, 64, 8]."""
         import numpy as np
         g = self.kernel_info(index)["grid"]
-        buf = np.zeros((g, 64, 8), dtype=np.int64)
+        buf = np.zeros((g, 64, 16), dtype=np.int64)
         _check(load_library().tm_exec_trace(self._h, index, buf.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)),
                                             buf.size))
         return buf

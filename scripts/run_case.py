@@ -62,7 +62,13 @@ def main():
         B = W.RESNET_BATCH
         cl = not a.nchw
         fmt = torch.channels_last if cl else torch.contiguous_format
-        ins = [rnd((B, L.c, L.h, L.h)).contiguous(memory_format=fmt),
+        if L.c < 8 and cl:  # 16-byte padded channels-last (NHWC8) view, TMA-able
+            xb = torch.zeros((B, L.h, L.h, 8), device=dev, dtype=torch.bfloat16)
+            xb[..., :L.c] = rnd((B, L.h, L.h, L.c))
+            x0 = xb.as_strided((B, L.c, L.h, L.h), (L.h * L.h * 8, 1, L.h * 8, 8))
+        else:
+            x0 = rnd((B, L.c, L.h, L.h)).contiguous(memory_format=fmt)
+        ins = [x0,
                rnd((L.f, L.c, L.k, L.k)).contiguous(memory_format=fmt), rnd((L.f,), torch.float32),
                rnd((L.f,), torch.float32)]
         ho = L.out_hw()
@@ -89,11 +95,12 @@ def main():
         ex.launch()
         torch.cuda.synchronize()
         tr = ex.trace(0)
-        names = ["prodF", "prodL", "mmaF", "mmaL", "epiRdy", "epiAcc", "epiDone"]
+        names = ["prodF", "prodL", "mmaF", "mmaL", "epiRdy", "epiAcc", "epiDone", "-", "ldS", "ldW", "ep0", "st0",
+                 "ep1", "st1"]
         for cta in (0, 1, tr.shape[0] - 1):
             print(f"CTA {cta} (cycles):")
             for i in range(64):
-                row = tr[cta, i, :7]
+                row = tr[cta, i, :14]
                 if not row.any():
                     continue
                 print(f"  tile {i:2d} " + " ".join(f"{n}={v:7d}" for n, v in zip(names, row)))

@@ -19,6 +19,14 @@ def dev(a, dtype="bf16", layout=None):
     x = t.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(tdt)
     if layout == "cl":
         x = x.contiguous(memory_format=t.channels_last)
+    elif layout == "cl8":
+        # NCHW logical view over a 16-byte padded channels-last buffer [N, H, W, 8];
+        # the pad channels hold NaN to prove they are never read (TMA zero-fills them)
+        n, c, h, w = x.shape
+        buf = t.full((n, h, w, 8), float("nan"), dtype=tdt)
+        buf[..., :c] = x.permute(0, 2, 3, 1)
+        buf = buf.cuda()
+        return buf.as_strided((n, c, h, w), (h * w * 8, 1, w * 8, 8))
     elif layout == "t":
         x = x.transpose(-1, -2).contiguous().transpose(-1, -2)
     return x.cuda()

@@ -178,6 +178,29 @@ def test_conv_bn_relu_exact(geom, layout, bm):
         assert np.array_equal(got["Z"], ref["Z"])
 
 
+@pytest.mark.parametrize("geom", [(2, 3, 20, 20, 64, 7, 7, 2, 3), (1, 3, 17, 19, 32, 3, 3, 1, 1),
+                                  (2, 4, 9, 9, 16, 5, 5, 2, 2)])
+def test_conv_small_channel_tma8_exact(geom):
+    """conv1-style C <= 8 on 16-byte padded channels-last input: one TMA im2col box per
+    tap (LD_IM2COL_TMA8, no-swizzle UMMA layout); pad channels are NaN in memory."""
+    n, c, h, w, f, kh, kw, s, p = geom
+    rng = port.Rng(6)
+    x = rng.tensor((n, c, h, w), True)
+    wt = rng.tensor((f, c, kh, kw), True)
+    scale, shift = rng.tensor((f,), True), rng.tensor((f,), True)
+    dag = conv_bn_relu_dag(n, c, h, w, f, kh, kw, s, p, DType.I32)
+    ho, wo = port.conv_out_extent(h, kh, s, p), port.conv_out_extent(w, kw, s, p)
+    import torch
+    from paper_2210_09603_b200 import Plan
+    xs = dev(x, layout="cl8")
+    out = torch.empty((n, f, ho, wo), dtype=torch.float32, device="cuda")
+    ex = Plan(dag).bind([xs, dev(wt, layout="cl"), dev(scale, "f32"), dev(shift, "f32")], [out])
+    assert ex.kernel_info(0)["a_loader"] == 6  # LD_IM2COL_TMA8
+    ex.launch()
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy().astype(np.float64), port.conv_bn_relu(x, wt, scale, shift, s, p))
+
+
 def test_conv_float_channels_last_output():
     """Float conv with the output bound channels-last (epilogue remap from the output's strides)."""
     import torch

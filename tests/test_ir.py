@@ -1,0 +1,131 @@
+"""Host-side IR parity with the reference (CPU only): builders, classify
+(fusion legality), DAG validation, partition and the fused-kernel plans."""
+import json
+import os
+
+import pytest
+
+import oracle
+from paper_2210_09603_b200 import (Axis, ComputeDAG, DType, OpClass, Plan, ScheduleConfig, TaskmapError, TensorNode,
+                                   classify, load, matmul_dag, partition, var, workloads)
+from paper_2210_09603_b200 import taskmap as T
+
+from dags import batched_matmul_scale_dag, conv_bn_relu_dag, ffn_dag, matmul_epilogue_dag
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+META = json.load(open(os.path.join(HERE, "golden", "golden.json")))
+
+
+@pytest.mark.parametrize("key", sorted(META["builders"]))
+def test_builders_match_reference(key):
+    """Same DAG structure and expression trees as compute_ir.cpp:496-733."""
+    kind, args = key.split(":")
+    args = [int(a) for a in args.split(",")]
+    mine = json.loads(T._build(kind, args).to_json())
+    ref = json.loads(META["builders"][key])
+    assert mine == ref
+
+
+@pytest.mark.parametrize("case", META["classify"], ids=[c["name"] for c in META["classify"]])
+def test_classify_matches_reference(case):
+    """classify (compute_ir.cpp:222-243) decides fusion legality: must agree exactly."""
+    dag = ComputeDAG.from_json(case["dag"])
+    assert int(classify(dag, case["node"])) == case["class"]
+
+
+def test_classify_probe_decisions():
+    """matmul C reduction; conv Col/Wf injective; Out bijective; reshape split
+    bijective but merge injective; transpose and BN bijective."""
+    conv = T.conv2d_im2col_dag(2, 3, 6, 6, 4, 3, 3, 1, 1)
+    assert [classify(conv, n) for n in ("Col", "Wf", "Y", "Out")] == [
+        OpClass.Injective, OpClass.Injective, OpClass.Reduction, OpClass.Bijective]
+    assert classify(T.reshape_dag([100], [2, 50]), "Y") == OpClass.Bijective
+    assert classify(T.reshape_dag([2, 50], [100]), "Y") == OpClass.Injective
+    assert classify(T.transpose_dag([2, 3, 4, 5], [0, 2, 1, 3]), "Y") == OpClass.Bijective
+
+
+def test_validate_errors_match_reference():
+    bad = [
+        ComputeDAG([TensorNode("X", [4]), TensorNode("X", [4], kind="compute", axes=[Axis("i", 4)],
+                                                     value=load("X", [var("i")]))], ["X"], ["X"]),
+        ComputeDAG([TensorNode("Y", [4], kind="compute", axes=[Axis("i", 4)], value=load("Z", [var("i")]))], [], ["Y"]),
+        ComputeDAG([TensorNode("X", [4]), TensorNode("Y", [4], kind="compute", axes=[Axis("i", 4)],
+                                                     value=load("X", [var("j")]))], ["X"], ["Y"]),
+        ComputeDAG([TensorNode("X", [4]), TensorNode("Y", [4], kind="compute", axes=[Axis("i", 3)],
+                                                     value=load("X", [var("i")]))], ["X"], ["Y"]),
+    ]
+    for d in bad:
+        with pytest.raises(TaskmapError) as mine:
+            classify(d, d.nodes[-1].name)
+        if oracle.ref_available():
+            with pytest.raises(oracle.RefError) as ref:
+                oracle.ref_validate(d.to_json())
+            assert str(mine.value) == str(ref.value)
+
+
+def test_partition_config_chains():
+    """Conv->BN->ReLU is one subgraph (im2col + filter prologues,
+    reshape + BN/ReLU epilogue); the FFN chain is two anchors."""
+    p = partition(conv_bn_relu_dag(1, 3, 8, 8, 4, 3, 3, 1, 1))
+    assert p == [{"anchor": "Y", "prologue": ["Wf", "Col"], "epilogue": ["Out", "Z"], "output": "Z"}]
+    p = partition(ffn_dag(8, 16, 32))
+    assert [s["anchor"] for s in p] == ["H0", "O0"] and p[0]["epilogue"] == ["H"] and p[1]["epilogue"] == ["O"]
+    p = partition(matmul_epilogue_dag(4, 4, 4))
+    assert p == [{"anchor": "C", "prologue": [], "epilogue": ["D"], "output": "D"}]
+
+
+def test_plans_lower_config_chains():
+    """Fused-kernel plans (no GPU needed to plan): loaders, epilogue programs, remaps."""
+    d = Plan(conv_bn_relu_dag(2, 64, 8, 8, 64, 3, 3, 1, 1)).describe()["kernels"][0]
+    assert d["A"] == "im2col(X)" and d["B"] == "filter(W)"
+    assert [o["kind"] for o in d["ops"]] == [19, 16, 32]      # MUL_T Scale, ADD_T Shift, RELU
+    d = Plan(batched_matmul_scale_dag(6, 128, 128, 64)).describe()["kernels"][0]
+    assert d["batch"] == 6 and [o["kind"] for o in d["ops"]] == [4]  # MUL_C 0.125
+    d = Plan(ffn_dag(64, 32, 128)).describe()
+    assert len(d["kernels"]) == 2 and d["intermediates"] == ["H"]
+    assert [o["kind"] for o in d["kernels"][0]["ops"]] == [16, 33]   # bias, GELU (tanh form matched)
+    assert [o["kind"] for o in d["kernels"][1]["ops"]] == [16, 16]   # bias, residual
+
+
+def test_fig11_prologue_epilogue_remap():
+    """PAPER Fig. 11 / SPEC.md:376,385: A[99-i] -> C[99-i]*2 prologue is a pure re-index of
+    an input; the epilogue stores y*3 at (i/50, i%50)."""
+    from paper_2210_09603_b200 import fimm, mul, sub, imm, div, mod
+    d = ComputeDAG()
+    d.add_input("C", [100, 8])
+    d.add_input("B", [8, 4])
+    d.nodes.append(TensorNode("A", [100, 8], kind="compute", axes=[Axis("i", 100), Axis("k", 8)],
+                              value=load("C", [sub(imm(99), var("i")), var("k")])))
+    d.nodes.append(TensorNode("Y", [100, 4], kind="reduce", axes=[Axis("i", 100), Axis("j", 4)],
+                              reduce_axes=[Axis("k", 8)], value=mul(load("A", [var("i"), var("k")]),
+                                                                     load("B", [var("k"), var("j")]))))
+    d.nodes.append(TensorNode("D", [2, 50, 4], kind="compute", axes=[Axis("a", 2), Axis("b", 50), Axis("j", 4)],
+                              value=mul(load("Y", [T.add(mul(var("a"), imm(50)), var("b")), var("j")]), fimm(3.0))))
+    d.outputs = ["D"]
+    assert partition(d) == [{"anchor": "Y", "prologue": ["A"], "epilogue": ["D"], "output": "D"}]
+    k = Plan(d).describe()["kernels"][0]
+    assert k["A"].startswith("C[99 - __row") and [o["kind"] for o in k["ops"]] == [4]
+
+
+def test_schedule_space_size_and_agnostic():
+    """50 <= |space| <= 200, identical for every shape."""
+    from paper_2210_09603_b200 import schedule_space
+    s = schedule_space("matmul")
+    assert 50 <= len(s) <= 200
+    assert s == schedule_space("conv2d")
+    assert len({(c.block_m, c.block_n, c.split_k, c.pipeline, c.raster) for c in s}) == len(s)
+
+
+def test_unsupported_reports_unsupported_status():
+    d = ComputeDAG()
+    d.add_input("X", [4, 4])
+    d.nodes.append(TensorNode("Y", [4], kind="reduce", axes=[Axis("i", 4)], reduce_axes=[Axis("j", 4)],
+                              combiner=T.Combiner.Max, value=load("X", [var("i"), var("j")])))
+    d.outputs = ["Y"]
+    with pytest.raises(TaskmapError) as e:
+        Plan(d)
+    assert "sum reductions" in str(e.value)
+
+
+def test_workload_flops():
+    assert abs(sum(L.flops(32) * L.count for L in workloads.RESNET50) / 1e9 - 261.6) < 0.1
