@@ -80,6 +80,12 @@ tm_status tm_mapping_text(const tm_mapping* m, int visualize, char** out);
 tm_status tm_mapping_lowered_assign(const tm_mapping* m, uint64_t worker, uint64_t* buf,
                                     size_t cap, size_t* n_tasks);
 
+/* Task lists of the compile-time mappings compiled into the fp32 CUDA-core
+ * kernel (0: compute spatial(4,2)*repeat(2,2)*spatial(4,8)*repeat(4,4),
+ * 1: A-tile load repeat(4,1)*spatial(32,8), 2: B-tile load
+ * repeat(1,4)*spatial(8,32)), evaluated on the host. */
+tm_status tm_kernel_mapping_assign(int32_t which, uint64_t worker, uint64_t* buf, size_t cap, size_t* n_tasks);
+
 /* ---- compute DAG: ComputeDAG / classify (compute_ir.hpp:39-56) ---- */
 /* classify (compute_ir.hpp:56): 0 reduction, 1 injective, 2 bijective */
 tm_status tm_classify(const char* dag_json, const char* node, int32_t* op_class);
@@ -113,7 +119,7 @@ int32_t tm_exec_num_launches(const tm_exec* e);
 tm_status tm_exec_kernel_info(const tm_exec* e, int32_t index, int32_t* grid, int32_t* cta_group,
                               int32_t* block_n, int32_t* split_k, int32_t* a_loader, int32_t* b_loader);
 /* Per-tile role timeline of kernel `index` (exec created with TMB_TRACE=1 in the
- * environment): [grid][64 tiles][8 events] int64 clock64 deltas; see TraceEv. */
+ * environment): [grid][64 tiles][16 events] int64 clock64 deltas; see TraceEv. */
 tm_status tm_exec_trace(const tm_exec* e, int32_t index, int64_t* buf, size_t cap);
 /* bind + launch (+ destroy) in one call. */
 tm_status tm_plan_launch(const tm_plan* p, const tm_tensor* inputs, int32_t n_in,

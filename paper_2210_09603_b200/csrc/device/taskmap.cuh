@@ -33,20 +33,21 @@ namespace tm {
 template <int... D>
 struct Dims {
   static constexpr int rank = sizeof...(D);
-  static constexpr int v[rank] = {D...};
-  static constexpr int volume() {
-    int p = 1;
-    for (int i = 0; i < rank; ++i) p *= v[i];
-    return p;
+  // extent of dimension i (a function, not a static array: usable in device code)
+  TMB_HD static constexpr int get(int i) {
+    int k = 0, r = 1;
+    ((k++ == i ? (r = D, 0) : 0), ...);
+    return r;
   }
+  TMB_HD static constexpr int volume() { return (1 * ... * D); }
 };
 
 // row-major unlinearisation of `flat` over D
 template <class D>
 TMB_HD constexpr void unflatten(uint32_t flat, int* out) {
   for (int i = D::rank - 1; i >= 0; --i) {
-    out[i] = static_cast<int>(flat % static_cast<uint32_t>(D::v[i]));
-    flat /= static_cast<uint32_t>(D::v[i]);
+    out[i] = static_cast<int>(flat % static_cast<uint32_t>(D::get(i)));
+    flat /= static_cast<uint32_t>(D::get(i));
   }
 }
 
@@ -56,7 +57,7 @@ struct Repeat {
   static constexpr int rank = dims_t::rank;
   static constexpr uint32_t workers = 1;
   static constexpr uint32_t tasks = dims_t::volume();
-  TMB_HD static constexpr int dim(int i) { return dims_t::v[i]; }
+  TMB_HD static constexpr int dim(int i) { return dims_t::get(i); }
   TMB_HD static constexpr void task(uint32_t /*w*/, uint32_t i, int* coord) {
     unflatten<dims_t>(i, coord);
   }
@@ -68,7 +69,7 @@ struct Spatial {
   static constexpr int rank = dims_t::rank;
   static constexpr uint32_t workers = dims_t::volume();
   static constexpr uint32_t tasks = 1;
-  TMB_HD static constexpr int dim(int i) { return dims_t::v[i]; }
+  TMB_HD static constexpr int dim(int i) { return dims_t::get(i); }
   TMB_HD static constexpr void task(uint32_t w, uint32_t /*i*/, int* coord) {
     unflatten<dims_t>(w, coord);
   }

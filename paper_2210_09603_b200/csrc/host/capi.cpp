@@ -184,6 +184,18 @@ tm_status tm_mapping_lowered_assign(const tm_mapping* m, uint64_t worker, uint64
   });
 }
 
+tm_status tm_kernel_mapping_assign(int32_t which, uint64_t worker, uint64_t* buf, size_t cap, size_t* n) {
+  return guarded([&] {
+    std::vector<int> tmp(4096);
+    const int k = tmb::kernel_mapping_assign(which, static_cast<uint32_t>(worker), tmp.data(), 4096);
+    if (k < 0) fail("bad kernel mapping id or worker");
+    if (static_cast<size_t>(2 * k) > cap) fail("buffer too small");
+    for (int i = 0; i < 2 * k; ++i) buf[i] = static_cast<uint64_t>(tmp[i]);
+    if (n) *n = static_cast<size_t>(k);
+    return TM_OK;
+  });
+}
+
 // ----------------------------------------------------------------- DAG --
 tm_status tm_classify(const char* dag_json, const char* node, int32_t* cls) {
   return guarded([&] {

@@ -765,7 +765,15 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
     std::string math = plan.cfg.math;
     const tm_tensor* opa = sp.a.kind == OperandPlan::Strided ? &lookup(env, sp.a.addr.tensor) : &lookup(env, sp.a.conv.x_tensor);
     const tm_tensor* opb = sp.b.kind == OperandPlan::Strided ? &lookup(env, sp.b.addr.tensor) : &lookup(env, sp.b.conv.w_tensor);
-    if (math == "auto") math = (opa->dtype == TM_F32 || opb->dtype == TM_F32) ? "tf32" : "bf16";
+    // auto: bf16 operands -> tcgen05 kind::f16; fp32 operands keep fp32 semantics on
+    // the CUDA-core kernel (matrix operands) or run kind::tf32 (convolutions);
+    // tf32 for matrices is an explicit choice (math="tf32")
+    if (math == "auto") {
+      if (opa->dtype == TM_F32 || opb->dtype == TM_F32)
+        math = (sp.a.kind == OperandPlan::Strided && sp.b.kind == OperandPlan::Strided) ? "fp32_simt" : "tf32";
+      else
+        math = "bf16";
+    }
     if (math == "fp32_simt") k.simt = 1;
     k.tf32 = math == "tf32";
     const int BK = k.tf32 ? 32 : 64;
@@ -914,9 +922,18 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
     };
     // SM-pair (cta_group::2, 256-row tiles) when requested and every operand is TMA-fed
     k.cg = 1;
-    if (plan.cfg.block_m == 256 && (k.bn == 128 || k.bn == 256) && bind_operands(2)) k.cg = 2;
+    if (!k.simt && plan.cfg.block_m == 256 && (k.bn == 128 || k.bn == 256) && bind_operands(2)) k.cg = 2;
     else bind_operands(1);
     p.tiles_m = static_cast<int32_t>((sp.M + 128 * k.cg - 1) / (128 * k.cg));
+    if (k.simt) {
+      // fp32 CUDA-core kernel (simt_fp32.cu): 128x128 tiles, strided predicated loads
+      if (p.a_loader == LD_IM2COL_GATHER || p.a_loader == LD_IM2COL_TMA || p.a_loader == LD_IM2COL_TMA8 ||
+          p.b_loader == LD_FILTER_GATHER || sp.b.kind == OperandPlan::ConvFilter)
+        fail("math=fp32_simt supports matrix operands only (conv im2col is not supported on this path)");
+      k.bn = 128;
+      p.tiles_n = static_cast<int32_t>((sp.N + 127) / 128);
+      p.tiles_m = static_cast<int32_t>((sp.M + 127) / 128);
+    }
     // ---- epilogue
     if (sp.ops.size() > static_cast<size_t>(kMaxEpiOps)) fail("epilogue longer than ", kMaxEpiOps, " ops");
     p.n_ops = static_cast<int32_t>(sp.ops.size());
@@ -995,7 +1012,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
     p.fast_math = p.out_dtype != TM_F32;  // approximate tanh only where the output rounding dominates
     // split-K: every split gets a non-empty k-block range
     {
-      int s = std::max(1, std::min(plan.cfg.split_k, p.num_kb));
+      int s = k.simt ? 1 : std::max(1, std::min(plan.cfg.split_k, p.num_kb));
       p.kb_per_split = (p.num_kb + s - 1) / s;
       p.split_k = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
       if (p.split_k > 1) {

@@ -95,6 +95,8 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
 int num_sms(int device);
 void launch_bound(const BoundKernel& k, void* stream);
 void pack_filter(const ConvGeom& g, int kp, void* out);  // bf16 [f][kp] in the GEMM K order
+void launch_simt(const BoundKernel& k, void* stream);   // fp32 CUDA-core kernel (simt_fp32.cu)
+int kernel_mapping_assign(int which, uint32_t worker, int* buf, int cap);
 unsigned long long device_mismatch(const void* a, const void* b, size_t bytes, void* stream);
 float device_max_rel_error(const void* a, const void* b, size_t n, int dtype, void* stream);
 void make_tma_2d3d(void* map, const void* ptr, int dtype, int rank, const uint64_t* dims,

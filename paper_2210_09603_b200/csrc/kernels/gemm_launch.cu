@@ -186,7 +186,10 @@ float device_max_rel_error(const void* a, const void* b, size_t n, int dtype, vo
 void launch_bound(const BoundKernel& k, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   bool ok;
-  if (k.cg == 2) ok = launch_cg2(k, s);
+  if (k.simt) {
+    launch_simt(k, stream);
+    ok = true;
+  } else if (k.cg == 2) ok = launch_cg2(k, s);
   else if (k.tf32) ok = launch_cg1_generic_tf32(k, s);
   else if (!k.generic) ok = launch_cg1_fast(k, s);
   else ok = launch_cg1_generic_bf16(k, s);

@@ -1,0 +1,33 @@
+"""Batch-sharded multi-GPU driver helpers (north star (4)).
+
+Every BASELINE workload is a map over its batch axis (images, tokens, heads),
+so ranks process disjoint batch slices with no collective during compute; the
+only exchange is one final gather of the result shards to rank 0.  One process
+per GPU, torch.distributed for the plumbing (NCCL on GPUs, gloo on CPU).
+"""
+from typing import List, Optional, Sequence, Tuple
+
+
+def shard_range(total: int, rank: int, world: int) -> Tuple[int, int]:
+    """[start, end) of rank's slice of `total` batch units (as even as possible)."""
+    if world <= 0 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} / world {world}")
+    base, extra = divmod(total, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def gather_to_root(shards: Sequence, dst: int = 0) -> Optional[List[list]]:
+    """Gathers each tensor in `shards` from every rank to `dst` (torch.distributed.gather).
+    Shapes must agree across ranks (weak scaling: equal per-rank batches).
+    Returns, on dst, one list of per-rank tensors per input; None elsewhere."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size()
+    rank = dist.get_rank()
+    out = []
+    for t in shards:
+        bufs = [torch.empty_like(t) for _ in range(world)] if rank == dst else None
+        dist.gather(t.contiguous(), bufs, dst=dst)
+        out.append(bufs)
+    return out if rank == dst else None

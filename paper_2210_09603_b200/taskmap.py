@@ -69,6 +69,7 @@ def load_library():
         "tm_mapping_assign": ([P, U64, ctypes.POINTER(U64), SZ, ctypes.POINTER(SZ)], I32),
         "tm_mapping_lowered_assign": ([P, U64, ctypes.POINTER(U64), SZ, ctypes.POINTER(SZ)], I32),
         "tm_mapping_text": ([P, ctypes.c_int, ctypes.POINTER(P)], I32),
+        "tm_kernel_mapping_assign": ([I32, U64, ctypes.POINTER(U64), SZ, ctypes.POINTER(SZ)], I32),
         "tm_classify": ([ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(I32)], I32),
         "tm_partition": ([ctypes.c_char_p, ctypes.POINTER(P)], I32),
         "tm_build_dag": ([ctypes.c_char_p, ctypes.POINTER(I64), I32, ctypes.POINTER(P)], I32),

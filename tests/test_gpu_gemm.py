@@ -126,6 +126,29 @@ def test_matmul_gelu_epilogue():
     assert port.max_rel_error(got["D"], want) <= 1e-4
 
 
+def test_fp32_config1_cuda_core_path():
+    """config 1: fp32 matmul M=N=K=1024 + bias + ReLU, unrounded U(-1,1) fp32 inputs, on the
+    task-mapped CUDA-core kernel (math auto -> fp32_simt): max_rel_error <= 1e-4."""
+    m = n = k = 1024
+    rng = port.Rng(1)
+    a, b, bias = rounded(rng.tensor((m, k)), "f32"), rounded(rng.tensor((k, n)), "f32"), rounded(rng.tensor((n,)), "f32")
+    dag = matmul_epilogue_dag(m, n, k)
+    got, plan = run(dag, {"A": dev(a, "f32"), "B": dev(b, "f32"), "Bias": dev(bias, "f32")}, {"D": (m, n)})
+    assert port.max_rel_error(got["D"], port.matmul_bias_relu(a, b, bias)) <= 1e-4
+
+
+@pytest.mark.parametrize("mnk", [(256, 256, 256), (2039, 67, 131), (1, 1, 1)])
+def test_fp32_cuda_core_exact_int(mnk):
+    m, n, k = mnk
+    a, b, bias = _matmul_case(m, n, k, True, 8)
+    dag = matmul_epilogue_dag(m, n, k, DType.I32)
+    got, _ = run(dag, {"A": dev(a, "f32"), "B": dev(b, "f32"), "Bias": dev(bias, "f32")}, {"D": (m, n)},
+                 cfg=ScheduleConfig(math="fp32_simt"))
+    want = oracle_eval(dag, {"A": a, "B": b, "Bias": bias}, {"D": (m, n)}) if (have_ref() and m * n * k < 2e7) \
+        else {"D": port.matmul_bias_relu(a, b, bias)}
+    assert np.array_equal(got["D"], want["D"])
+
+
 def test_matmul_tf32():
     m, n, k = 512, 384, 256
     rng = port.Rng(12)

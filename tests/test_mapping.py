@@ -94,6 +94,25 @@ def test_coverage_bijection_200_compositions():
         assert set(seen) == set(itertools.product(*[range(d) for d in m.task_shape]))
 
 
+@pytest.mark.parametrize("which,text", [
+    (0, "spatial(4, 2) * repeat(2, 2) * spatial(4, 8) * repeat(4, 4)"),
+    (1, "repeat(4, 1) * spatial(32, 8)"),
+    (2, "repeat(1, 4) * spatial(8, 32)")])
+def test_kernel_compiled_mappings_equal_reference_assign(which, text):
+    """The compile-time (constexpr) mappings inside the fp32 CUDA-core kernel produce
+    exactly the task lists of the reference's assign() for the same mapping text."""
+    import ctypes
+    from paper_2210_09603_b200.taskmap import load_library
+    lib = load_library()
+    ref = oracle.ref_mapping_assign if oracle.ref_available() else (lambda t, w: TaskMapping(t).assign(w))
+    for w in range(256):
+        buf = (ctypes.c_uint64 * 4096)()
+        n = ctypes.c_size_t()
+        assert lib.tm_kernel_mapping_assign(which, w, buf, 4096, ctypes.byref(n)) == 0
+        got = [(buf[2 * i], buf[2 * i + 1]) for i in range(n.value)]
+        assert got == [tuple(t) for t in ref(text, w)]
+
+
 def test_lowering_equals_assign_random_chains():
     """the closed-form per-worker index (device DevMapping) equals assign()."""
     rng = random.Random(17)
