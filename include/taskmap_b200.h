@@ -125,6 +125,17 @@ tm_status tm_exec_trace(const tm_exec* e, int32_t index, int64_t* buf, size_t ca
 tm_status tm_plan_launch(const tm_plan* p, const tm_tensor* inputs, int32_t n_in,
                          const tm_tensor* outputs, int32_t n_out, void* cuda_stream);
 
+/* CUDA graph of a sequence of bound execs (e.g. every layer of a network), replayed
+ * with one launch: removes the per-kernel host launch cost. The execs must outlive
+ * the graph (it references their buffers). timed != 0 records an event before each
+ * exec and after the last, read back with tm_graph_exec_ms (per-exec ms of the most
+ * recent launch, after the stream is synchronised). */
+typedef struct tm_graph tm_graph;
+tm_status tm_graph_create(const tm_exec* const* execs, int32_t n, int32_t timed, tm_graph** out);
+tm_status tm_graph_launch(const tm_graph* g, void* cuda_stream);
+tm_status tm_graph_exec_ms(const tm_graph* g, float* ms, int32_t n);
+void tm_graph_destroy(tm_graph* g);
+
 /* tune: enumerate the space on the bound tensors, time each
  * config with CUDA events, gate on agreement with the default config, pick
  * the fastest (ties: space order). Report JSON (TuneReport). */

@@ -53,7 +53,13 @@ struct EpiOp {
 constexpr int kMaxEpiOps = 8;
 constexpr int kMaxMatOps = 2;
 constexpr int kTraceTiles = 64;
-constexpr int kTraceEvents = 16;  // 0-7 role events (TraceEv), 8-13 fine epilogue ticks
+constexpr int kTraceEvents = 16;  // 0-7 role events (TraceEv); tile 0: 14/15 = setup done / exit (ns)
+
+// Output staging of the epilogue: each epilogue warp owns one smem buffer of
+// 32 rows x out_stage_row_bytes (a 64- or 128-byte swizzled row segment per
+// lane), written to global memory by one TMA store per column group.  64-byte
+// rows for BN = 256 single-CTA tiles, whose pipeline needs the shared memory.
+constexpr int out_stage_row_bytes(int bn, int cg) { return (bn == 256 && cg == 1) ? 64 : 128; }
 // trace events per tile
 enum TraceEv : int32_t {
   TR_PROD_FIRST = 0,  // producer: first k-block slot acquired
@@ -131,10 +137,12 @@ struct GemmParams {
   int32_t canon_s_op;      // op index providing S (-1: constant canon_s)
   int32_t canon_t_op;      // op index providing T (-1: constant canon_t)
   int32_t canon_res_slot;  // SIDE_MAT prefetch slot added after the activation (-1: none)
+  int32_t canon_res_op;    // op index of that residual (-1: none)
   float canon_s, canon_t;
   // optional per-tile role timeline (clock64 relative to CTA start), layout
   // [cta][kTraceTiles][kTraceEvents]; null = tracing off
   long long* trace;
+  int32_t dbg;  // diagnostics (TMB_DBG): 1 = skip all roles after setup
   int32_t n_ops;
   int32_t has_mat;  // any SIDE_MAT op
   int32_t out_dtype;

@@ -15,8 +15,8 @@
 //     list (bias / scale / BN-fold / ReLU / GELU / residual ...) and store
 //     through the epilogue's output address map (NCHW re-index etc.).
 //
-// Warp roles (13 warps): 0-3 loaders, 4-11 epilogue (TMEM lane group = warp%4,
-// interleaved 16-column chunks), 12 MMA issuer + TMEM owner.
+// Warp roles (13 warps): 0-3 loaders, 4-11 epilogue (two groups of 4, one per
+// TMEM accumulator buffer; TMEM lane group = warp%4), 12 MMA issuer + TMEM owner.
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -28,13 +28,13 @@ namespace tmb {
 
 constexpr int kBM = 128;          // tile rows (TMEM lanes)
 constexpr int kRowBytes = 128;    // one swizzle-128B row of K
-constexpr int kEpiWarps = 8;       // epilogue warps (2 per TMEM lane group)
+constexpr int kEpiWarps = 8;       // epilogue warps (2 groups x 4 TMEM lane groups)
 constexpr int kNumThreads = 32 * (4 + kEpiWarps + 1);  // loaders + epilogue + MMA
 
 // CG = CTAs per MMA (cta_group): 1, or 2 for the SM-pair form where the tile
 // is (2*128) x BN, each CTA stages its 128 rows of A and BN/2 rows of B, and
 // the pair leader issues tcgen05.mma.cta_group::2 over both CTAs' smem.
-template <int BN, int STAGES, bool TF32, int CG = 1>
+template <int BN, int STAGES, bool TF32, int CG = 1, bool GENERIC = true>
 struct GemmCfg {
   static constexpr int kElem = TF32 ? 4 : 2;
   static constexpr int BK = kRowBytes / kElem;        // 64 bf16 / 32 tf32
@@ -44,12 +44,26 @@ struct GemmCfg {
   static constexpr int B_BYTES = (BN / CG) * kRowBytes;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
-  static constexpr int COLBUF_BYTES = kMaxEpiOps * BN * 4;  // staged per-column epilogue operands
-  static constexpr int OUTBUF_BYTES = kEpiWarps * 32 * 16 * 4;  // per-warp 32x16 output chunk (<= f32)
-  static constexpr int SMEM_BYTES =
-      STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + COLBUF_BYTES + OUTBUF_BYTES;
+  // per epilogue warp group (one per TMEM accumulator): staged per-column operands
+  static constexpr int COL_OPS = GENERIC ? kMaxEpiOps : 2;
+  static constexpr int COLBUF_BYTES = 2 * COL_OPS * BN * 4;
+  static constexpr int OUT_ROW = out_stage_row_bytes(BN, CG);      // bytes per lane per column group
+  static constexpr int OUTBUF_BYTES = kEpiWarps * 32 * OUT_ROW;  // one staging buffer per epilogue warp
+  // layout: [STAGES x (A | B)] [outbuf] [barriers 256 B] [colbuf]; the base is
+  // 1024-byte aligned (checked at run time) as SWIZZLE_128B requires
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + OUTBUF_BYTES + 256 + COLBUF_BYTES;
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 must be 16..256 step 16");
 };
+
+constexpr int kMaxSmem = 232448;  // 227 KB opt-in dynamic shared memory per CTA on sm_100
+
+// deepest ring (<= 8 stages) that fits next to the epilogue buffers
+constexpr int stages_for(int bn, int cg, bool generic = true) {
+  const int stage = kBM * kRowBytes + (bn / cg) * kRowBytes;
+  const int fixed = kEpiWarps * 32 * out_stage_row_bytes(bn, cg) + 256 + 2 * (generic ? kMaxEpiOps : 2) * bn * 4;
+  const int n = (kMaxSmem - fixed) / stage;
+  return n > 8 ? 8 : n;
+}
 
 namespace detail {
 
@@ -249,6 +263,12 @@ __device__ __forceinline__ void bf16x8_to_f32(const uint4 u, float* o) {
   }
 }
 
+// strided / unaligned / ragged-edge fallback, one element per call and kept out
+// of line (rare, and large once unrolled; scalar arguments stay in registers)
+static __device__ __noinline__ float load_mat1(const void* ptr, int64_t idx, int32_t dt, bool ok) {
+  return ok ? load_side(ptr, idx, dt) : 0.f;
+}
+
 // 16 consecutive columns of a matrix side operand for one row (vectorised
 // when contiguous and 16-byte aligned, otherwise predicated scalar loads).
 __device__ __forceinline__ void load_mat16(const EpiOp& op, int64_t rowpart, int64_t col0, int N,
@@ -277,8 +297,7 @@ __device__ __forceinline__ void load_mat16(const EpiOp& op, int64_t rowpart, int
     }
   }
 #pragma unroll
-  for (int j = 0; j < 16; ++j)
-    out[j] = (col0 + j < N) ? load_side(op.ptr, base + j * op.a.s_col, op.dtype) : 0.f;
+  for (int j = 0; j < 16; ++j) out[j] = load_mat1(op.ptr, base + j * op.a.s_col, op.dtype, col0 + j < N);
 }
 
 // Applies the fused epilogue op list to 16 consecutive columns of one row.
@@ -350,6 +369,9 @@ __device__ __forceinline__ void apply_epilogue(const GemmParams& p, float (&v)[1
   }
 }
 
+// exp-based GELU (fp32 outputs), out of line: rare, and large unrolled 16x
+static __device__ __noinline__ float gelu_precise1(float x) { return gelu_tanh(x); }
+
 // Canonical epilogue: v = act(acc * S[c] + T[c]) (+ R), S/T staged in smem.
 template <int BN>
 __device__ __forceinline__ void apply_canon(const GemmParams& p, float (&v)[16], const float* colbuf, int cbase,
@@ -373,7 +395,7 @@ __device__ __forceinline__ void apply_canon(const GemmParams& p, float (&v)[16],
       for (int j = 0; j < 16; ++j) v[j] = gelu_tanh_fast(v[j]);
     } else {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = gelu_tanh(v[j]);
+      for (int j = 0; j < 16; ++j) v[j] = gelu_precise1(v[j]);
     }
   }
   if (p.canon_res_slot == 0) {
@@ -399,14 +421,22 @@ __device__ __forceinline__ void epilogue16(const GemmParams& p, float (&v)[16], 
   }
 }
 
+// one element of any output dtype (scalar fallback of store_out, out of line)
+static __device__ __noinline__ void store1(void* out, int32_t dt, int64_t idx, float x) {
+  if (dt == DT_BF16) reinterpret_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(x);
+  else if (dt == DT_F32) reinterpret_cast<float*>(out)[idx] = x;
+  else reinterpret_cast<__half*>(out)[idx] = __float2half_rn(x);
+}
+
+// direct (non-TMA) store of 16 columns of one row
 __device__ __forceinline__ void store_out(const GemmParams& p, const float (&v)[16], int64_t base,
                                           int64_t col0, bool row_ok) {
   if (!row_ok) return;
   const int64_t sc = p.out_a.s_col;
-  const bool full = col0 + 16 <= p.N;
-  if (p.out_dtype == DT_BF16) {
+  const bool full = col0 + 16 <= p.N && sc == 1;
+  if (full && p.out_dtype == DT_BF16) {
     __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(p.out);
-    if (sc == 1 && full && ((reinterpret_cast<uintptr_t>(o + base + col0) & 15) == 0)) {
+    if ((reinterpret_cast<uintptr_t>(o + base + col0) & 15) == 0) {
       uint32_t w[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -416,27 +446,119 @@ __device__ __forceinline__ void store_out(const GemmParams& p, const float (&v)[
       uint4* dst = reinterpret_cast<uint4*>(o + base + col0);
       dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
       dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (col0 + j < p.N) o[base + (col0 + j) * sc] = __float2bfloat16_rn(v[j]);
+      return;
     }
-  } else if (p.out_dtype == DT_F32) {
+  } else if (full && p.out_dtype == DT_F32) {
     float* o = reinterpret_cast<float*>(p.out);
-    if (sc == 1 && full && ((reinterpret_cast<uintptr_t>(o + base + col0) & 15) == 0)) {
+    if ((reinterpret_cast<uintptr_t>(o + base + col0) & 15) == 0) {
       float4* dst = reinterpret_cast<float4*>(o + base + col0);
 #pragma unroll
       for (int j = 0; j < 4; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (col0 + j < p.N) o[base + (col0 + j) * sc] = v[j];
+      return;
     }
-  } else {
-    __half* o = reinterpret_cast<__half*>(p.out);
+  }
+  // strided (e.g. NCHW: lanes = consecutive pixels, still coalesced) or ragged
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
-      if (col0 + j < p.N) o[base + (col0 + j) * sc] = __float2half_rn(v[j]);
+  for (int j = 0; j < 16; ++j)
+    if (col0 + j < p.N) store1(p.out, p.out_dtype, base + (col0 + j) * sc, v[j]);
+}
+
+// Fast-path drain of one accumulator tile for one warp (32 rows x ncols):
+// canonical epilogue v = act(acc * S[c] + T[c]) (+ R[row, c]) with the
+// activation / residual fixed at compile time, so each 32-column step is
+// straight-line code: TMEM load (x32) -> FMA with the staged S/T -> act ->
+// (+ bf16 residual, prefetched one step ahead) -> bf16 pack -> swizzled smem
+// staging -> one TMA store per OUT_ROW-byte column group.  The accumulator is
+// handed back to the MMA right after the last TMEM load.
+template <int BN, int CG, int OUT_ROW, int ACT, bool RES>
+__device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t taddr, const float* colbuf,
+                                           uint8_t* obuf, int ncols, int32_t col_base, int32_t row0,
+                                           int32_t b, int lane, const uint4* res, uint64_t* tempty_bar,
+                                           long long* tr, long long t0) {
+  constexpr int GC = OUT_ROW / 2;  // bf16 columns per TMA store group (32 or 64)
+  // optional fine timeline of the first two steps (tr != null: one warp, one tile)
+  auto tick = [&](int c, int ev) {
+    if (tr != nullptr && lane == 0 && (c == 0 || ev == 13)) tr[ev] = clock64() - t0;
+  };
+  uint4 rq[4];
+  if constexpr (RES) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) rq[q] = __ldg(res + q);
+  }
+#pragma unroll 1
+  for (int c = 0; c < ncols; c += 32) {
+    uint32_t r[32];
+    tick(c, 8);
+    ptx::tmem_ld32(taddr + c, r);
+    uint4 rn[4];
+    if constexpr (RES) {
+      if (c + 32 < ncols) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rn[q] = __ldg(res + (c + 32) / 8 + q);
+      }
+    }
+    ptx::tmem_wait_ld();
+    tick(c, 9);
+    if (c + 32 >= ncols) {  // last TMEM read of this tile: the MMA may reuse the buffer
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (CG == 2) ptx::mbar_arrive_remote(ptx::mapa_shared(ptx::smem_u32(tempty_bar), 0));
+        else ptx::mbar_arrive(tempty_bar);
+      }
+    }
+    if (c % GC == 0) {  // the previous store from this buffer has read it
+      if (lane == 0) ptx::bulk_wait_read<0>();
+      __syncwarp();
+    }
+    tick(c, 10);
+    uint32_t w[16];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 sv = *reinterpret_cast<const float4*>(colbuf + c + 4 * q);
+      const float4 tv = *reinterpret_cast<const float4*>(colbuf + BN + c + 4 * q);
+      float x[4] = {fmaf(__uint_as_float(r[4 * q]), sv.x, tv.x), fmaf(__uint_as_float(r[4 * q + 1]), sv.y, tv.y),
+                    fmaf(__uint_as_float(r[4 * q + 2]), sv.z, tv.z), fmaf(__uint_as_float(r[4 * q + 3]), sv.w, tv.w)};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if constexpr (ACT == 1) x[j] = fmaxf(x[j], 0.f);
+        if constexpr (ACT == 2) x[j] = gelu_tanh_fast(x[j]);
+      }
+      if constexpr (RES) {  // bf16 elements 4q .. 4q+3 of the 32: words 2q, 2q+1 of rq[]
+        const uint32_t* rw = reinterpret_cast<const uint32_t*>(rq);
+        const uint32_t w0 = rw[2 * q], w1 = rw[2 * q + 1];
+        x[0] += __uint_as_float(w0 << 16);
+        x[1] += __uint_as_float(w0 & 0xFFFF0000u);
+        x[2] += __uint_as_float(w1 << 16);
+        x[3] += __uint_as_float(w1 & 0xFFFF0000u);
+      }
+      __nv_bfloat162 h0 = __floats2bfloat162_rn(x[0], x[1]);
+      __nv_bfloat162 h1 = __floats2bfloat162_rn(x[2], x[3]);
+      w[2 * q] = *reinterpret_cast<uint32_t*>(&h0);
+      w[2 * q + 1] = *reinterpret_cast<uint32_t*>(&h1);
+    }
+    const int j0 = (c % GC) / 8;  // 16-byte chunk of this lane's staged row
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint32_t a = static_cast<uint32_t>(lane * OUT_ROW + (j0 + k) * 16);
+      a ^= ((a >> 7) & (OUT_ROW == 128 ? 7u : 3u)) << 4;  // the TMA store's swizzle
+      *reinterpret_cast<uint4*>(obuf + a) = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+    }
+    tick(c, 11);
+    if (c == 32) tick(c, 13);
+    if ((c + 32) % GC == 0 || c + 32 >= ncols) {
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        ptx::tma_store_3d(tmC, obuf, col_base + (c / GC) * GC, row0, b);
+        ptx::bulk_commit();
+      }
+    }
+    tick(c, 12);
+    if constexpr (RES) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) rq[q] = rn[q];
+    }
   }
 }
 
@@ -452,7 +574,7 @@ __device__ __forceinline__ bool next_tile(const GemmParams& p, uint32_t i, int& 
                                           int& tn, bool& valid) {
   if (i >= p.tile_map.tasks) return false;
   int32_t c[tm::kMaxRank];
-  tm::dev_task(p.tile_map, blockIdx.x / CG, i, c);  // workers = CTA pairs when CG == 2
+  tm::dev_task_fixed<2, 3>(p.tile_map, blockIdx.x / CG, i, c);  // workers = CTA pairs when CG == 2
   b = c[0] / p.split_k;
   ks = c[0] % p.split_k;
   tm_ = c[1];
@@ -467,24 +589,25 @@ template <int BN, int STAGES, bool TF32, int CG, bool GENERIC>
 __global__ void __launch_bounds__(kNumThreads, 1)
     tm_gemm_kernel(const __grid_constant__ GemmParams p, const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmC) {
-  using Cfg = GemmCfg<BN, STAGES, TF32, CG>;
+  using Cfg = GemmCfg<BN, STAGES, TF32, CG, GENERIC>;
   constexpr int BK = Cfg::BK;
   constexpr int kTileM = kBM * CG;  // rows per tile (both CTAs of a pair)
   const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0u;
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw = ptx::smem_u32(smem_raw);
-  uint8_t* smem = smem_raw + ((1024u - (raw & 1023u)) & 1023u);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if ((ptx::smem_u32(smem_raw) & 1023u) != 0u) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
+  uint8_t* smem = smem_raw;
   uint8_t* smA = smem;
   uint8_t* smB = smem + STAGES * Cfg::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE_BYTES);
+  uint8_t* outbuf = smem + STAGES * Cfg::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(outbuf + Cfg::OUTBUF_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint32_t* split_flag = tmem_slot + 1;
-  float* colbuf = reinterpret_cast<float*>(smem + STAGES * Cfg::STAGE_BYTES + 256);
-  uint8_t* outbuf = smem + STAGES * Cfg::STAGE_BYTES + 256 + Cfg::COLBUF_BYTES;
+  uint32_t* split_flag = tmem_slot + 1;  // [2], one per epilogue warp group
+  float* colbuf_all = reinterpret_cast<float*>(outbuf + Cfg::OUTBUF_BYTES + 256);
 
+  const uint64_t gt_entry = p.trace != nullptr ? ptx::globaltimer() : 0;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const bool a_tma = p.a_loader == LD_TMA_K || p.a_loader == LD_IM2COL_TMA || p.a_loader == LD_IM2COL_TMA8;
@@ -500,7 +623,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], kEpiWarps * CG);  // both CTAs' epilogues drain before reuse
+      ptx::mbar_init(&tempty[a], 4 * CG);  // the group's 4 warps (of both CTAs) drained it
     }
     ptx::fence_mbar_init();
   }
@@ -514,11 +637,15 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   const long long t0 = clock64();
-  if (p.trace != nullptr && threadIdx.x == 0)
-    p.trace[static_cast<int64_t>(blockIdx.x) * kTraceTiles * kTraceEvents + TR_CTA_START] =
-        static_cast<long long>(ptx::globaltimer());
+  if (p.trace != nullptr && threadIdx.x == 0) {  // ns: kernel entry, setup done (tile 0's slots 7, 14)
+    long long* tr0 = p.trace + static_cast<int64_t>(blockIdx.x) * kTraceTiles * kTraceEvents;
+    tr0[TR_CTA_START] = static_cast<long long>(gt_entry);
+    tr0[14] = static_cast<long long>(ptx::globaltimer());
+  }
 
-  if (warp < 4) {
+  if (p.dbg == 1) {
+    // diagnostics: setup + teardown only
+  } else if (warp < 4) {
     // ===================== loaders (prologue splice) =====================
     const int t = threadIdx.x;  // 0..127
     if (all_tma && t != 0) {
@@ -644,12 +771,19 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
   } else if (warp < 4 + kEpiWarps) {
     // ===================== epilogue (epilogue splice) =====================
-    const int e = warp - 4;          // 0..7
-    const int lg = warp & 3;         // TMEM lane group this warp may access
-    const int half = e >> 2;         // which interleaved half of the 16-column chunks
-    const int et = threadIdx.x - 128;
+    // Two warp groups, one per TMEM accumulator buffer: group h drains the
+    // CTA's tiles 1 mod 2 == h, so two tiles' epilogues overlap and each warp
+    // (TMEM lane group lg = warp % 4: rows lg*32 .. +32 of the tile) walks the
+    // whole tile width.  Output columns go out in groups of OUT_ROW bytes per
+    // row: 32 rows are staged in this warp's swizzled smem buffer and written
+    // by one TMA store.
+    const int e = warp - 4;                // 0..7
+    const int lg = warp & 3;               // TMEM lane group this warp may access
+    const int grp = e >> 2;                // warp group = accumulator buffer it drains
+    const int gt = threadIdx.x - 128 - grp * 128;  // thread index within the group (0..127)
+    const bool lead = (e & 3) == 0 && lane == 0;  // traces / counters
     constexpr int kChunks = BN / 16;
-    int acc = 0;
+    float* colbuf = colbuf_all + grp * (Cfg::COL_OPS * BN);
     uint32_t acc_phase = 0;
     int b, ks, tm_, tn;
     bool valid;
@@ -658,23 +792,23 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     bool has_col = false;
     for (int o = 0; o < p.n_ops; ++o) has_col = has_col || p.ops[o].side == SIDE_COL;
     int staged_tn = -1, staged_b = -1;
-    // this warp's 32x16 output staging: 2 KB, a 2-deep ring of 1 KB bf16 chunks
-    // (one outstanding TMA store while the next chunk is written) or one f32 chunk
-    uint8_t* obuf_base = outbuf + e * (32 * 16 * 4);
+    uint8_t* obuf = outbuf + e * (32 * Cfg::OUT_ROW);
     const int obytes = p.out_dtype == DT_F32 ? 4 : 2;
-    uint32_t n_emit = 0;
-    auto emit = [&](const float (&v)[16], int64_t obase_, int64_t col0, bool row_ok_, int tile_row0) {
+    const int gcols = Cfg::OUT_ROW / obytes;  // columns per TMA-store group
+    // 16-byte chunk j of this lane's staged row, with the TMA swizzle applied
+    auto stage_at = [&](int j) -> uint4* {
+      uint32_t a = static_cast<uint32_t>(lane * Cfg::OUT_ROW + j * 16);
+      a ^= ((a >> 7) & (Cfg::OUT_ROW == 128 ? 7u : 3u)) << 4;
+      return reinterpret_cast<uint4*>(obuf + a);
+    };
+    // 16 finished columns (tile column c) -> staging buffer or global memory
+    auto put16 = [&](const float (&v)[16], int c, int64_t obase_, int64_t n0_, bool row_ok_) {
+      if (p.dbg == 2) return;  // diagnostics: no output stores
       if (!p.out_tma) {
-        detail::store_out(p, v, obase_, col0, row_ok_);
+        detail::store_out(p, v, obase_, n0_ + c, row_ok_);
         return;
       }
-      uint8_t* obuf = obuf_base + (obytes == 2 ? (n_emit & 1u) * 1024 : 0);
-      if (lane == 0) {  // the store that last used this buffer has read it
-        if (obytes == 2) ptx::bulk_wait_read<1>();
-        else ptx::bulk_wait_read<0>();
-      }
-      ++n_emit;
-      __syncwarp();
+      const int j0 = (c % gcols) * obytes / 16;
       if (obytes == 2) {
         uint32_t w[8];
 #pragma unroll
@@ -682,14 +816,23 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
           w[j] = *reinterpret_cast<uint32_t*>(&h);
         }
-        uint4* dst = reinterpret_cast<uint4*>(obuf + lane * 32);
-        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        *stage_at(j0) = make_uint4(w[0], w[1], w[2], w[3]);
+        *stage_at(j0 + 1) = make_uint4(w[4], w[5], w[6], w[7]);
       } else {
-        float4* dst = reinterpret_cast<float4*>(obuf + lane * 64);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        for (int q = 0; q < 4; ++q)
+          *stage_at(j0 + q) = make_uint4(__float_as_uint(v[4 * q]), __float_as_uint(v[4 * q + 1]),
+                                         __float_as_uint(v[4 * q + 2]), __float_as_uint(v[4 * q + 3]));
       }
+    };
+    // before the first put16 of a column group: the previous store has read the buffer
+    auto group_begin = [&]() {
+      if (!p.out_tma) return;
+      if (lane == 0) ptx::bulk_wait_read<0>();
+      __syncwarp();
+    };
+    auto group_end = [&](int64_t col0, int tile_row0) {
+      if (!p.out_tma || p.dbg == 2) return;
       ptx::fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) {
@@ -697,54 +840,77 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         ptx::bulk_commit();
       }
     };
+    auto release_acc = [&]() {
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        // the (leader's) MMA may overwrite this accumulator once both CTAs drained it
+        if constexpr (CG == 2) ptx::mbar_arrive_remote(ptx::mapa_shared(ptx::smem_u32(&tempty[grp]), 0));
+        else ptx::mbar_arrive(&tempty[grp]);
+      }
+    };
+    uint32_t nvalid = 0;
     for (uint32_t i = 0; detail::next_tile<CG>(p, i, b, ks, tm_, tn, valid); ++i) {
       if (!valid) continue;
+      if ((nvalid++ & 1u) != static_cast<uint32_t>(grp)) continue;  // the other group's tile
       const int64_t n0 = static_cast<int64_t>(tn) * BN;
-      const int row0 = tm_ * kTileM + rank * kBM + lg * 32;  // this warp's first row
+      const int tile_row0 = tm_ * kTileM + rank * kBM;
+      const int row0 = tile_row0 + lg * 32;  // this warp's first row
       const int64_t row = static_cast<int64_t>(row0) + lane;
       const bool row_ok = row < p.M;
       const int64_t rr = row_ok ? row : 0;
       // Stage this tile's column vectors while the MMA works on it; skipped when
-      // the previous tile had the same columns (e.g. every tile of a conv whose
-      // F fits one tile), which keeps the load latency off the critical path.
+      // the group's previous tile had the same columns (e.g. every tile of a conv
+      // whose F fits one tile), which keeps the load latency off the critical path.
       const bool restage = (staged_tn < 0 && (has_col || p.canon)) || (has_col && (tn != staged_tn || b != staged_b));
-      if (restage) ptx::named_bar_sync(1, 32 * kEpiWarps);  // previous tile's readers are done
+      if (restage) ptx::named_bar_sync(1 + grp, 128);  // the group's previous readers are done
       if (restage && p.canon) {  // S and T column vectors of the canonical epilogue
-        for (int c = et; c < BN; c += 32 * kEpiWarps) {
+        for (int c = gt; c < BN; c += 128) {
           const bool in = n0 + c < p.N;
-          float s = p.canon_s, t = p.canon_t;
+          float sv = p.canon_s, tv = p.canon_t;
           if (p.canon_s_op >= 0 && in) {
             const EpiOp& op = p.ops[p.canon_s_op];
-            s = detail::load_side(op.ptr, detail::addr_rowpart(op.a, 0, b) + (n0 + c) * op.a.s_col, op.dtype);
+            sv = detail::load_side(op.ptr, detail::addr_rowpart(op.a, 0, b) + (n0 + c) * op.a.s_col, op.dtype);
           }
           if (p.canon_t_op >= 0 && in) {
             const EpiOp& op = p.ops[p.canon_t_op];
-            t = detail::load_side(op.ptr, detail::addr_rowpart(op.a, 0, b) + (n0 + c) * op.a.s_col, op.dtype);
+            tv = detail::load_side(op.ptr, detail::addr_rowpart(op.a, 0, b) + (n0 + c) * op.a.s_col, op.dtype);
           }
-          colbuf[c] = s;
-          colbuf[BN + c] = t;
+          colbuf[c] = sv;
+          colbuf[BN + c] = tv;
         }
       }
-      for (int o = 0; o < p.n_ops; ++o) {
-        const EpiOp& op = p.ops[o];
-        rowpart[o] = detail::addr_rowpart(op.a, rr, b);
-        if (op.side == SIDE_COL && restage && !p.canon) {
-          const int64_t cb = detail::addr_rowpart(op.a, 0, b);
-          for (int c = et; c < BN; c += 32 * kEpiWarps)
-            colbuf[o * BN + c] = (n0 + c < p.N) ? detail::load_side(op.ptr, cb + (n0 + c) * op.a.s_col, op.dtype) : 0.f;
-        } else if (op.side == SIDE_ROW) {
-          rowv[o] = row_ok ? detail::load_side(op.ptr, rowpart[o], op.dtype) : 0.f;
+      if constexpr (GENERIC) {
+#pragma unroll 1
+        for (int o = 0; o < p.n_ops; ++o) {
+          const EpiOp& op = p.ops[o];
+          rowpart[o] = detail::addr_rowpart(op.a, rr, b);
+          if (op.side == SIDE_COL && restage && !p.canon) {
+            const int64_t cb = detail::addr_rowpart(op.a, 0, b);
+            for (int c = gt; c < BN; c += 128)
+              colbuf[o * BN + c] = (n0 + c < p.N) ? detail::load_side(op.ptr, cb + (n0 + c) * op.a.s_col, op.dtype) : 0.f;
+          } else if (op.side == SIDE_ROW) {
+            rowv[o] = row_ok ? detail::load_side(op.ptr, rowpart[o], op.dtype) : 0.f;
+          }
         }
+      } else if (p.canon_res_op >= 0) {  // canonical form: the residual is the only per-element operand
+        rowpart[0] = detail::addr_rowpart(p.ops[p.canon_res_op].a, rr, b);
       }
-      const int64_t obase = detail::addr_rowpart(p.out_a, rr, b);
+      const int64_t obase = p.out_tma ? 0 : detail::addr_rowpart(p.out_a, rr, b);
       if (restage) {
-        ptx::named_bar_sync(1, 32 * kEpiWarps);  // column buffers ready
+        ptx::named_bar_sync(1 + grp, 128);  // column buffers ready
         staged_tn = tn;
         staged_b = b;
       }
-      if (et == 0) detail::trace(p, i, TR_EPI_READY, t0);
+      if (lead) detail::trace(p, i, TR_EPI_READY, t0);
       float mat[kMaxMatOps][16];
       auto prefetch = [&](int c, float (&dst)[kMaxMatOps][16]) {
+        if constexpr (!GENERIC) {
+          if (p.canon_res_op >= 0)  // slot 0: the canonical form has one matrix operand
+            detail::load_mat16(p.ops[p.canon_res_op], rowpart[0], n0 + c * 16, p.N, row_ok, dst[0]);
+          return;
+        }
+#pragma unroll 1
         for (int o = 0; o < p.n_ops; ++o)
           if (p.ops[o].side == SIDE_MAT) {
             float tmp[16];
@@ -756,19 +922,21 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             }
           }
       };
-      if (p.has_mat && p.split_k == 1) prefetch(2 * half, mat);
-      if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&tfull[acc], acc_phase);
-      else ptx::mbar_wait(&tfull[acc], acc_phase);
+      if (GENERIC && p.has_mat && p.split_k == 1) prefetch(0, mat);
+      if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&tfull[grp], acc_phase);
+      else ptx::mbar_wait(&tfull[grp], acc_phase);
+      acc_phase ^= 1u;
       ptx::tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lg * 32) << 16) + acc * BN;
-      if (et == 0) detail::trace(p, i, TR_EPI_ACC, t0);
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lg * 32) << 16) + grp * BN;
+      if (lead) detail::trace(p, i, TR_EPI_ACC, t0);
+      const int ncols = static_cast<int>(min(static_cast<int64_t>(BN), p.N - n0));  // valid columns
       if (p.split_k > 1) {
         // ---- split-K: park the raw partial tile, last unit reduces + runs the epilogue
         const int64_t tile_id = ((static_cast<int64_t>(b) * p.tiles_m + tm_) * p.tiles_n + tn) * CG + rank;
         const float* ws = p.workspace + tile_id * p.split_k * static_cast<int64_t>(kBM * BN);
         const int rloc = lg * 32 + lane;
 #pragma unroll 1
-        for (int c = half; c < kChunks; c += 2) {
+        for (int c = 0; c < kChunks; ++c) {
           uint32_t r[16];
           ptx::tmem_ld16(taddr + c * 16, r);
           ptx::tmem_wait_ld();
@@ -780,29 +948,22 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             __stcg(dst + q, make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
                                         __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
         }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {  // TMEM is free again: the MMA can start the next unit
-          if constexpr (CG == 2) ptx::mbar_arrive_remote(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
-          else ptx::mbar_arrive(&tempty[acc]);
-        }
-        if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+        release_acc();  // TMEM is free again: the MMA can start the next unit
         __threadfence();
-        ptx::named_bar_sync(2, 32 * kEpiWarps);
-        if (et == 0) *split_flag = (atomicAdd(&p.counters[tile_id], 1) == p.split_k - 1) ? 1u : 0u;
-        ptx::named_bar_sync(2, 32 * kEpiWarps);
-        if (*reinterpret_cast<volatile uint32_t*>(split_flag) == 0u) continue;
+        ptx::named_bar_sync(3 + grp, 128);
+        if (gt == 0) split_flag[grp] = (atomicAdd(&p.counters[tile_id], 1) == p.split_k - 1) ? 1u : 0u;
+        ptx::named_bar_sync(3 + grp, 128);
+        if (*reinterpret_cast<volatile uint32_t*>(&split_flag[grp]) == 0u) continue;
         __threadfence();
 #pragma unroll 1
-        for (int c = half; c < kChunks; c += 2) {
-          const int64_t col0 = n0 + c * 16;
-          if (col0 >= p.N) break;
+        for (int c = 0; c * 16 < ncols; ++c) {
+          if (c % (gcols / 16) == 0) group_begin();
           if (p.has_mat) prefetch(c, mat);
           float v[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) v[j] = 0.f;
-          for (int s = 0; s < p.split_k; ++s) {  // fixed order: deterministic
-            const float4* src = reinterpret_cast<const float4*>(ws + s * static_cast<int64_t>(kBM * BN) +
+          for (int sp = 0; sp < p.split_k; ++sp) {  // fixed order: deterministic
+            const float4* src = reinterpret_cast<const float4*>(ws + sp * static_cast<int64_t>(kBM * BN) +
                                                                 (static_cast<int64_t>(c) * kBM + rloc) * 16);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -811,60 +972,67 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             }
           }
           detail::epilogue16<BN, GENERIC>(p, v, colbuf, c * 16, rowv, mat);
-          emit(v, obase, col0, row_ok, row0);
+          put16(v, c * 16, obase, n0, row_ok);
+          if ((c + 1) % (gcols / 16) == 0 || (c + 1) * 16 >= ncols)
+            group_end(n0 + (c * 16 / gcols) * gcols, row0);
         }
-        if (et == 0) p.counters[tile_id] = 0;  // self-resetting for the next launch
+        if (gt == 0) p.counters[tile_id] = 0;  // self-resetting for the next launch
         continue;
       }
-      // 32 columns per TMEM round trip (one wait per 32 columns); the two warps
-      // of a lane group interleave 32-column chunks
+      // 32 columns per TMEM load; the accumulator is released right after the
+      // last load, before the math of the last columns
+      if constexpr (!GENERIC) {
+        // compact variant (host guarantees: canonical epilogue, bf16 TMA-stored
+        // output, residual absent or bf16 contiguous 16-byte aligned with N % 32 == 0)
+        const uint4* res = nullptr;
+        if (p.canon_res_op >= 0)
+          res = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.ops[p.canon_res_op].ptr) +
+                                               rowpart[0] + n0);
+        const int32_t cb = static_cast<int32_t>(n0);
+        long long* ftr = (p.trace != nullptr && e == 0 && i < static_cast<uint32_t>(kTraceTiles))
+                             ? p.trace + (static_cast<int64_t>(blockIdx.x) * kTraceTiles + i) * kTraceEvents
+                             : nullptr;
+        switch (p.canon_act * 2 + (res != nullptr ? 1 : 0)) {
+#define TMB_DRAIN(A, R)                                                                                          \
+  case A * 2 + R:                                                                                                \
+    detail::drain_fast<BN, CG, Cfg::OUT_ROW, A, R>(&tmC, taddr, colbuf, obuf, ncols, cb, row0, b, lane, res,      \
+                                                   &tempty[grp], ftr, t0);                                       \
+    break;
+          TMB_DRAIN(0, 0) TMB_DRAIN(0, 1) TMB_DRAIN(1, 0) TMB_DRAIN(1, 1) TMB_DRAIN(2, 0) TMB_DRAIN(2, 1)
+#undef TMB_DRAIN
+          default: __trap();
+        }
+        if (lead) detail::trace(p, i, TR_EPI_DONE, t0);
+        continue;
+      }
 #pragma unroll 1
-      for (int c2 = half; c2 < BN / 32; c2 += 2) {
-        const int64_t colA = n0 + c2 * 32;
-        if (colA >= p.N) break;  // warp-uniform
-        float nxt[kMaxMatOps][16];
-        if (p.has_mat && colA + 16 < p.N) prefetch(2 * c2 + 1, nxt);
+      for (int c2 = 0; c2 * 32 < ncols; ++c2) {
         uint32_t r[32];
-        // fine-grained epilogue timeline: warp 4 of every CTA, first 32-column chunk
-        // of each tile -> trace events 8..13 (kTraceEvents = 16)
-        const bool fine = p.trace != nullptr && warp == 4 && c2 == half && i < static_cast<uint32_t>(kTraceTiles);
-        auto tick = [&](int ev) {
-          if (fine && lane == 0)
-            p.trace[(static_cast<int64_t>(blockIdx.x) * kTraceTiles + i) * kTraceEvents + ev] = clock64() - t0;
-        };
-        tick(8);
         ptx::tmem_ld32(taddr + c2 * 32, r);
         ptx::tmem_wait_ld();
-        tick(9);
-        {
+        if ((c2 + 1) * 32 >= ncols) release_acc();
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+          const int c = c2 * 32 + hh * 16;
+          if (c >= ncols) break;
+          if (c % gcols == 0) group_begin();
           float v[16];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-          detail::epilogue16<BN, GENERIC>(p, v, colbuf, c2 * 32, rowv, mat);
-          tick(10);
-          emit(v, obase, colA, row_ok, row0);
-          tick(11);
-        }
-        if (colA + 16 < p.N) {
-          float v[16];
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[hh * 16 + j]);
+          float nxt[kMaxMatOps][16];
+          if (p.has_mat && c + 16 < ncols) prefetch(c / 16 + 1, nxt);
+          detail::epilogue16<BN, GENERIC>(p, v, colbuf, c, rowv, mat);
+          put16(v, c, obase, n0, row_ok);
+          if (p.has_mat) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[16 + j]);
-          if (p.has_mat && c2 + 2 < BN / 32 && colA + 64 < p.N) prefetch(2 * (c2 + 2), mat);
-          detail::epilogue16<BN, GENERIC>(p, v, colbuf, c2 * 32 + 16, rowv, nxt);
-          tick(12);
-          emit(v, obase, colA + 16, row_ok, row0);
-          tick(13);
+            for (int o = 0; o < kMaxMatOps; ++o)
+#pragma unroll
+              for (int j = 0; j < 16; ++j) mat[o][j] = nxt[o][j];
+          }
+          if ((c + 16) % gcols == 0 || c + 16 >= ncols) group_end(n0 + (c / gcols) * gcols, row0);
         }
       }
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        // the (leader's) MMA may overwrite this accumulator once both CTAs drained it
-        if constexpr (CG == 2) ptx::mbar_arrive_remote(ptx::mapa_shared(ptx::smem_u32(&tempty[acc]), 0));
-        else ptx::mbar_arrive(&tempty[acc]);
-      }
-      if (et == 0) detail::trace(p, i, TR_EPI_DONE, t0);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
+      if (lead) detail::trace(p, i, TR_EPI_DONE, t0);
     }
     if (p.out_tma && lane == 0) ptx::bulk_wait<0>();  // all output tiles written before exit
   } else {
@@ -924,13 +1092,25 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
   }
 
+  if (p.trace != nullptr && lane == 0)  // ns: warp reached the final barrier (tile 2 + warp, slot 15)
+    p.trace[(static_cast<int64_t>(blockIdx.x) * kTraceTiles + 2 + warp) * kTraceEvents + 15] =
+        static_cast<long long>(ptx::globaltimer());
   ptx::tc_fence_before();
   if constexpr (CG == 2) ptx::cluster_sync();  // peer done with its TMEM before the pair frees it
   else __syncthreads();
+  if (p.trace != nullptr && threadIdx.x == 0)  // ns: all roles done (tile 0's slot 15)
+    p.trace[static_cast<int64_t>(blockIdx.x) * kTraceTiles * kTraceEvents + 15] =
+        static_cast<long long>(ptx::globaltimer());
   if (warp == 4 + kEpiWarps) {
+    if (p.trace != nullptr && lane == 0)  // ns: MMA warp past the barrier (tile 1's slot 14)
+      p.trace[(static_cast<int64_t>(blockIdx.x) * kTraceTiles + 1) * kTraceEvents + 14] =
+          static_cast<long long>(ptx::globaltimer());
     ptx::tc_fence_after();
     if constexpr (CG == 2) ptx::tmem_dealloc_2sm<Cfg::TMEM_COLS>(tmem_base);
     else ptx::tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+    if (p.trace != nullptr && lane == 0)  // ns: TMEM released (tile 1's slot 15)
+      p.trace[(static_cast<int64_t>(blockIdx.x) * kTraceTiles + 1) * kTraceEvents + 15] =
+          static_cast<long long>(ptx::globaltimer());
   }
 }
 

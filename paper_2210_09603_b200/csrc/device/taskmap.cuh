@@ -22,8 +22,10 @@
 
 #ifndef __CUDACC__
 #define TMB_HD
+#define TMB_UNROLL
 #else
 #define TMB_HD __host__ __device__
+#define TMB_UNROLL _Pragma("unroll")
 #endif
 
 namespace tmb {
@@ -138,6 +140,42 @@ TMB_HD inline void dev_task(const DevMapping& m, uint32_t w, uint32_t i, int32_t
       const uint32_t e = static_cast<uint32_t>(m.dims[a][d]);
       coord[d] += static_cast<int32_t>(flat % e) * scale[d];
       flat /= e;
+      scale[d] *= static_cast<int32_t>(e);
+    }
+  }
+}
+
+// dev_task for a chain whose atom count and rank are known at compile time
+// (the kernels' CTA -> tile mapping is always 2 atoms over rank 3): fully
+// unrolled, ~20 instructions per division instead of the generic loop nest,
+// which keeps the per-tile scheduler out of the instruction-cache budget.
+template <int NA, int R>
+TMB_HD inline void dev_task_fixed(const DevMapping& m, uint32_t w, uint32_t i, int32_t* coord) {
+  int32_t scale[R];
+TMB_UNROLL
+  for (int d = 0; d < R; ++d) {
+    coord[d] = 0;
+    scale[d] = 1;
+  }
+TMB_UNROLL
+  for (int a = NA - 1; a >= 0; --a) {
+    uint32_t vol = 1;
+TMB_UNROLL
+    for (int d = 0; d < R; ++d) vol *= static_cast<uint32_t>(m.dims[a][d]);
+    uint32_t flat;
+    if (m.is_spatial[a]) {
+      flat = w % vol;
+      w /= vol;
+    } else {
+      flat = i % vol;
+      i /= vol;
+    }
+TMB_UNROLL
+    for (int d = R - 1; d >= 0; --d) {
+      const uint32_t e = static_cast<uint32_t>(m.dims[a][d]);
+      const uint32_t q = flat / e;
+      coord[d] += static_cast<int32_t>(flat - q * e) * scale[d];
+      flat = q;
       scale[d] *= static_cast<int32_t>(e);
     }
   }

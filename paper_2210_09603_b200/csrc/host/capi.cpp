@@ -350,6 +350,77 @@ tm_status tm_exec_trace(const tm_exec* e, int32_t index, int64_t* buf, size_t ca
   });
 }
 
+// ---- CUDA graphs: a sequence of bound execs replayed with one launch ----
+struct tm_graph {
+  cudaGraphExec_t exec = nullptr;
+  std::vector<cudaEvent_t> marks;  // timed graphs: one event before each exec + one at the end
+  ~tm_graph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    for (auto ev : marks) cudaEventDestroy(ev);
+  }
+};
+
+tm_status tm_graph_create(const tm_exec* const* execs, int32_t n, int32_t timed, tm_graph** out) {
+  return guarded([&] {
+    if (!out || n < 0 || (n > 0 && !execs)) fail("tm_graph_create: bad arguments");
+    auto g = std::make_unique<tm_graph>();
+    auto ck = [](cudaError_t e, const char* what) {
+      if (e != cudaSuccess) fail(what, " failed: cuda error ", cudaGetErrorString(e));
+    };
+    if (timed) {
+      g->marks.resize(static_cast<size_t>(n) + 1);
+      for (auto& ev : g->marks) ck(cudaEventCreate(&ev), "cudaEventCreate");
+    }
+    cudaStream_t s;
+    ck(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+    cudaGraph_t graph = nullptr;
+    ck(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "cudaStreamBeginCapture");
+    try {
+      for (int32_t i = 0; i < n; ++i) {
+        if (!execs[i]) fail("tm_graph_create: null exec");
+        if (timed) ck(cudaEventRecordWithFlags(g->marks[i], s, cudaEventRecordExternal), "cudaEventRecord");
+        for (const auto& k : execs[i]->e->kernels) tmb::launch_bound(k, s);
+      }
+      if (timed) ck(cudaEventRecordWithFlags(g->marks[n], s, cudaEventRecordExternal), "cudaEventRecord");
+    } catch (...) {
+      cudaStreamEndCapture(s, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      cudaStreamDestroy(s);
+      throw;
+    }
+    ck(cudaStreamEndCapture(s, &graph), "cudaStreamEndCapture");
+    const cudaError_t ie = cudaGraphInstantiate(&g->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    cudaStreamDestroy(s);
+    ck(ie, "cudaGraphInstantiate");
+    *out = g.release();
+    return TM_OK;
+  });
+}
+
+tm_status tm_graph_launch(const tm_graph* g, void* stream) {
+  return guarded([&] {
+    if (!g) fail("null graph");
+    const cudaError_t e = cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) fail("cudaGraphLaunch failed: cuda error ", cudaGetErrorString(e));
+    return TM_OK;
+  });
+}
+
+tm_status tm_graph_exec_ms(const tm_graph* g, float* ms, int32_t n) {
+  return guarded([&] {
+    if (!g || g->marks.empty()) fail("tm_graph_exec_ms: graph was not created with timed = 1");
+    if (!ms || n != static_cast<int32_t>(g->marks.size()) - 1) fail("tm_graph_exec_ms: n must equal the exec count");
+    for (int32_t i = 0; i < n; ++i) {
+      const cudaError_t e = cudaEventElapsedTime(&ms[i], g->marks[i], g->marks[i + 1]);
+      if (e != cudaSuccess) fail("cudaEventElapsedTime failed: cuda error ", cudaGetErrorString(e));
+    }
+    return TM_OK;
+  });
+}
+
+void tm_graph_destroy(tm_graph* g) { delete g; }
+
 tm_status tm_plan_launch(const tm_plan* p, const tm_tensor* in, int32_t n_in, const tm_tensor* out, int32_t n_out,
                          void* stream) {
   return guarded([&] {
@@ -407,17 +478,32 @@ tm_status tm_tune(const char* dag_json, const tm_tensor* in, int32_t n_in, const
     auto run = [&](const ScheduleConfig& c, float& ms) {
       auto plan = tmb::build_plan(d, c, device);
       auto ex = tmb::bind_plan(*plan, in, n_in, out, n_out);
-      for (const auto& k : ex->kernels) tmb::launch_bound(k, s);  // warm-up
-      std::vector<float> times;
-      for (int r = 0; r < reps; ++r) {
-        cudaEventRecord(e0, s);
+      for (const auto& k : ex->kernels) tmb::launch_bound(k, s);  // warm-up (and the gated result)
+      if (cudaStreamSynchronize(s) != cudaSuccess) fail("cuda error while tuning: ", cudaGetErrorString(cudaGetLastError()));
+      // time `reps` back-to-back launches replayed from a CUDA graph: device time
+      // only, without the host launch cost that would otherwise dominate small shapes
+      cudaGraph_t graph = nullptr;
+      cudaGraphExec_t gexec = nullptr;
+      if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) fail("cuda capture failed in tune");
+      for (int r = 0; r < reps; ++r)
         for (const auto& k : ex->kernels) tmb::launch_bound(k, s);
+      if (cudaStreamEndCapture(s, &graph) != cudaSuccess || cudaGraphInstantiate(&gexec, graph, 0) != cudaSuccess) {
+        if (graph) cudaGraphDestroy(graph);
+        fail("cuda graph capture failed in tune: ", cudaGetErrorString(cudaGetLastError()));
+      }
+      cudaGraphDestroy(graph);
+      std::vector<float> times;
+      cudaGraphLaunch(gexec, s);  // warm
+      for (int r = 0; r < 3; ++r) {
+        cudaEventRecord(e0, s);
+        cudaGraphLaunch(gexec, s);
         cudaEventRecord(e1, s);
         cudaEventSynchronize(e1);
         float t = 0;
         cudaEventElapsedTime(&t, e0, e1);
-        times.push_back(t);
+        times.push_back(t / reps);
       }
+      cudaGraphExecDestroy(gexec);
       if (cudaStreamSynchronize(s) != cudaSuccess) fail("cuda error while tuning: ", cudaGetErrorString(cudaGetLastError()));
       std::sort(times.begin(), times.end());
       ms = times[times.size() / 2];

@@ -970,7 +970,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       const int n = p.n_ops;
       p.canon_s = 1.f;
       p.canon_t = 0.f;
-      p.canon_s_op = p.canon_t_op = p.canon_res_slot = -1;
+      p.canon_s_op = p.canon_t_op = p.canon_res_slot = p.canon_res_op = -1;
       auto is = [&](int kind) { return i < n && p.ops[i].kind == kind; };
       if (is(EPI_MUL_C)) { p.canon_s = p.ops[i].c; ++i; }
       else if (is(EPI_MUL_T) && p.ops[i].side == SIDE_COL) { p.canon_s_op = i; ++i; }
@@ -979,12 +979,8 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       else if (is(EPI_ADD_T) && p.ops[i].side == SIDE_COL) { p.canon_t_op = i; ++i; }
       if (is(EPI_RELU)) { p.canon_act = 1; ++i; }
       else if (is(EPI_GELU_TANH)) { p.canon_act = 2; ++i; }
-      if (is(EPI_ADD_T) && p.ops[i].side == SIDE_MAT) { p.canon_res_slot = p.ops[i].slot; ++i; }
+      if (is(EPI_ADD_T) && p.ops[i].side == SIDE_MAT) { p.canon_res_slot = p.ops[i].slot; p.canon_res_op = i; ++i; }
       p.canon = (i == n && !std::getenv("TMB_NO_CANON")) ? 1 : 0;
-      // compact instantiation when every operand is TMA-fed and the epilogue is canonical
-      const bool a_t = p.a_loader == LD_TMA_K || p.a_loader == LD_IM2COL_TMA || p.a_loader == LD_IM2COL_TMA8;
-      const bool b_t = p.b_loader == LD_TMA_K || p.b_loader == LD_TMA_MN;
-      k.generic = (a_t && b_t && p.canon && !k.tf32 && !std::getenv("TMB_GENERIC")) ? 0 : 1;
     }
     {
       const tm_tensor& t = lookup(env, sp.out.tensor);
@@ -993,10 +989,11 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       p.out = t.data;
       p.out_dtype = t.dtype;
       p.out_a = to_addr(f);
-      // Row-major (channels-last, [M,N]) outputs: the epilogue stages each
-      // 32x16 chunk in smem and TMA-stores it (coalesced, off the LSU).  Outputs
-      // whose rows are the contiguous dimension (NCHW) keep direct stores,
-      // which are already coalesced (lanes = consecutive pixels).
+      // Row-major (channels-last, [M,N]) outputs: each epilogue warp stages a
+      // 32-row x (64 or 128 byte) column group in swizzled smem and TMA-stores
+      // it (coalesced, off the LSU).  Outputs whose rows are the contiguous
+      // dimension (NCHW) keep direct stores, which are already coalesced (lanes
+      // = consecutive pixels).
       const int es = esize(t.dtype);
       const uintptr_t base = reinterpret_cast<uintptr_t>(t.data) + f.off * es;
       if (f.c1 == 1 && f.P >= sp.M && f.lo > 0 && (f.lo * es) % 16 == 0 && (f.c2 * es) % 16 == 0 && base % 16 == 0 &&
@@ -1004,9 +1001,29 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
         p.out_tma = 1;
         const uint64_t dims[3] = {(uint64_t)sp.N, (uint64_t)sp.M, (uint64_t)sp.batch};
         const uint64_t strides[2] = {(uint64_t)(f.lo * es), (uint64_t)(std::max<int64_t>(f.c2, f.lo * sp.M) * es)};
-        const uint32_t box[3] = {16u, 32u, 1u};
-        make_tma_2d3d(k.tma_c, reinterpret_cast<const void*>(base), t.dtype, 3, dims, strides, box, false);
+        const int rb = out_stage_row_bytes(k.bn, k.cg);
+        const uint32_t box[3] = {static_cast<uint32_t>(rb / es), 32u, 1u};
+        make_tma_2d3d(k.tma_c, reinterpret_cast<const void*>(base), t.dtype, 3, dims, strides, box, rb);
       }
+    }
+    {
+      // compact instantiation (drain_fast): TMA-fed operands, canonical epilogue,
+      // bf16 TMA-stored output, residual absent or bf16 / contiguous / 16-byte
+      // aligned rows with N % 32 == 0
+      const bool a_t = p.a_loader == LD_TMA_K || p.a_loader == LD_IM2COL_TMA || p.a_loader == LD_IM2COL_TMA8;
+      const bool b_t = p.b_loader == LD_TMA_K || p.b_loader == LD_TMA_MN;
+      bool res_ok = true;
+      if (p.canon && p.canon_res_op >= 0) {
+        const EpiOp& r = p.ops[p.canon_res_op];
+        const Addr& a = r.a;
+        res_ok = r.dtype == DT_BF16 && a.s_col == 1 && p.N % 32 == 0 &&
+                 reinterpret_cast<uintptr_t>(r.ptr) % 16 == 0 && (a.s_hi * 2) % 16 == 0 &&
+                 (a.s_lo * 2) % 16 == 0 && (a.s_batch * 2) % 16 == 0 && (a.offset * 2) % 16 == 0;
+      }
+      k.generic = (a_t && b_t && p.canon && !k.tf32 && p.out_tma && p.out_dtype == DT_BF16 && res_ok &&
+                   !std::getenv("TMB_GENERIC"))
+                      ? 0
+                      : 1;
     }
     if (const char* sw = std::getenv("TMB_MN_SWAP")) p.mn_lbo_sbo_swap = std::atoi(sw);
     p.fast_math = p.out_dtype != TM_F32;  // approximate tanh only where the output rounding dominates
@@ -1032,6 +1049,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
     int used = grid / k.cg;
     p.tile_map = tile_mapping(int64_t(sp.batch) * p.split_k, p.tiles_m, p.tiles_n, grid / k.cg, plan.cfg.raster, used);
     k.grid = used * k.cg;  // workers of the tile mapping are CTA pairs when cg == 2
+    if (const char* d = std::getenv("TMB_DBG")) p.dbg = std::atoi(d);
     if (std::getenv("TMB_TRACE")) {  // per-tile role timeline (tm_exec_trace)
       void* tr = nullptr;
       const size_t bytes = size_t(k.grid) * kTraceTiles * kTraceEvents * 8;

@@ -99,8 +99,9 @@ void launch_simt(const BoundKernel& k, void* stream);   // fp32 CUDA-core kernel
 int kernel_mapping_assign(int which, uint32_t worker, int* buf, int cap);
 unsigned long long device_mismatch(const void* a, const void* b, size_t bytes, void* stream);
 float device_max_rel_error(const void* a, const void* b, size_t n, int dtype, void* stream);
+// swizzle: smem swizzle span in bytes (0 = none, 64, 128)
 void make_tma_2d3d(void* map, const void* ptr, int dtype, int rank, const uint64_t* dims,
-                   const uint64_t* strides_bytes, const uint32_t* box, bool swizzle128 = true);
+                   const uint64_t* strides_bytes, const uint32_t* box, int swizzle = 128);
 void make_tma_im2col(void* map, const void* ptr, int dtype, const uint64_t* dims_cwhn,
                      const uint64_t* strides_bytes, int pad_lo, int pad_hi_corner, int stride,
                      uint32_t channels, uint32_t pixels, bool swizzle128 = true);

@@ -52,7 +52,7 @@ int num_sms(int device) {
 }
 
 void make_tma_2d3d(void* map, const void* ptr, int dtype, int rank, const uint64_t* dims,
-                   const uint64_t* strides_bytes, const uint32_t* box, bool swizzle128) {
+                   const uint64_t* strides_bytes, const uint32_t* box, int swizzle) {
   static EncodeTiled enc = driver_fn<EncodeTiled>("cuTensorMapEncodeTiled");
   cuuint64_t d[5];
   cuuint64_t s[4];
@@ -64,7 +64,9 @@ void make_tma_2d3d(void* map, const void* ptr, int dtype, int rank, const uint64
   }
   for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
   check_cu(enc(reinterpret_cast<CUtensorMap*>(map), tma_dtype(dtype), rank, const_cast<void*>(ptr), d, s, b,
-               e, CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+               e, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               swizzle == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                              : (swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE),
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
            "cuTensorMapEncodeTiled");
 }

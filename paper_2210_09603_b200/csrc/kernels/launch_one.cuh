@@ -11,16 +11,10 @@
 
 namespace tmb {
 
-// stage counts chosen to fill ~192 KB of shared memory (per-CTA stage bytes
-// are 16 KB of A + BN/CG rows of B)
-constexpr int stages_for(int bn, int cg) {
-  const int kb = 16 + bn / cg / 8;  // KB per stage
-  return (192 / kb) > 8 ? 8 : (192 / kb);
-}
-
 template <int BN, int STAGES, bool TF32, int CG, bool GENERIC>
 void launch_one(const BoundKernel& k, cudaStream_t s) {
-  using Cfg = GemmCfg<BN, STAGES, TF32, CG>;
+  using Cfg = GemmCfg<BN, STAGES, TF32, CG, GENERIC>;
+  static_assert(Cfg::SMEM_BYTES <= kMaxSmem, "shared memory budget");
   auto fn = tm_gemm_kernel<BN, STAGES, TF32, CG, GENERIC>;
   static bool attr_set = false;
   if (!attr_set) {

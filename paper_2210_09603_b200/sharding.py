@@ -17,17 +17,24 @@ def shard_range(total: int, rank: int, world: int) -> Tuple[int, int]:
     return start, start + base + (1 if rank < extra else 0)
 
 
-def gather_to_root(shards: Sequence, dst: int = 0) -> Optional[List[list]]:
-    """Gathers each tensor in `shards` from every rank to `dst` (torch.distributed.gather).
-    Shapes must agree across ranks (weak scaling: equal per-rank batches).
-    Returns, on dst, one list of per-rank tensors per input; None elsewhere."""
+def gather_buffers(shards: Sequence, dst: int = 0) -> Optional[List[list]]:
+    """Receive buffers for gather_to_root on `dst` (one per rank per shard); None elsewhere."""
     import torch
     import torch.distributed as dist
-    world = dist.get_world_size()
+    if dist.get_rank() != dst:
+        return None
+    return [[torch.empty_like(t) for _ in range(dist.get_world_size())] for t in shards]
+
+
+def gather_to_root(shards: Sequence, dst: int = 0, bufs: Optional[List[list]] = None) -> Optional[List[list]]:
+    """Gathers each tensor in `shards` from every rank to `dst` (torch.distributed.gather).
+    Shapes must agree across ranks (weak scaling: equal per-rank batches).
+    `bufs` (from gather_buffers) avoids allocating inside a timed loop.
+    Returns, on dst, one list of per-rank tensors per input; None elsewhere."""
+    import torch.distributed as dist
     rank = dist.get_rank()
-    out = []
-    for t in shards:
-        bufs = [torch.empty_like(t) for _ in range(world)] if rank == dst else None
-        dist.gather(t.contiguous(), bufs, dst=dst)
-        out.append(bufs)
-    return out if rank == dst else None
+    if bufs is None:
+        bufs = gather_buffers(shards, dst)
+    for i, t in enumerate(shards):
+        dist.gather(t.contiguous(), bufs[i] if rank == dst else None, dst=dst)
+    return bufs if rank == dst else None

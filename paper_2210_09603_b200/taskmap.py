@@ -84,6 +84,10 @@ def load_library():
         "tm_exec_kernel_info": ([P, I32] + [ctypes.POINTER(I32)] * 6, I32),
         "tm_exec_trace": ([P, I32, ctypes.POINTER(I64), SZ], I32),
         "tm_plan_launch": ([P, ctypes.POINTER(TmTensor), I32, ctypes.POINTER(TmTensor), I32, P], I32),
+        "tm_graph_create": ([ctypes.POINTER(P), I32, I32, ctypes.POINTER(P)], I32),
+        "tm_graph_launch": ([P, P], I32),
+        "tm_graph_exec_ms": ([P, ctypes.POINTER(ctypes.c_float), I32], I32),
+        "tm_graph_destroy": ([P], None),
         "tm_tune": ([ctypes.c_char_p, ctypes.POINTER(TmTensor), I32, ctypes.POINTER(TmTensor), I32, I32, I32,
                      ctypes.POINTER(TmScheduleConfig), ctypes.POINTER(P)], I32),
     }
@@ -503,6 +507,36 @@ class Exec:
     def __del__(self):
         if getattr(self, "_h", None) and _LIB is not None:
             _LIB.tm_exec_destroy(self._h)
+            self._h = None
+
+
+class Graph:
+    """A CUDA graph replaying a sequence of bound execs with one launch (tm_graph).
+
+    timed=True records an event around every exec; exec_ms() then returns the
+    per-exec device time (ms) of the most recent launch (after a synchronize)."""
+
+    def __init__(self, execs, timed: bool = False):
+        self._execs = list(execs)  # the graph references their buffers
+        arr = (ctypes.c_void_p * max(1, len(self._execs)))(*[e._h.value for e in self._execs])
+        h = ctypes.c_void_p()
+        _check(load_library().tm_graph_create(arr, len(self._execs), int(timed), ctypes.byref(h)))
+        self._h = h
+
+    def launch(self, stream=None):
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        _check(load_library().tm_graph_launch(self._h, ctypes.c_void_p(s.cuda_stream)))
+
+    def exec_ms(self):
+        n = len(self._execs)
+        buf = (ctypes.c_float * max(1, n))()
+        _check(load_library().tm_graph_exec_ms(self._h, buf, n))
+        return [buf[i] for i in range(n)]
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _LIB is not None:
+            _LIB.tm_graph_destroy(self._h)
             self._h = None
 
 

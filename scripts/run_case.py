@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--bt", action="store_true", help="store B K-major (transposed)")
     ap.add_argument("--f32out", action="store_true")
     ap.add_argument("--trace", action="store_true", help="print the per-tile role timeline of CTA 0/1")
+    ap.add_argument("--gap", action="store_true", help="globaltimer gap between two graph-chained launches")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     rnd = lambda s, dt=torch.bfloat16: torch.empty(s, device=dev).uniform_(-1, 1).to(dt)
@@ -76,17 +77,46 @@ def main():
         dag, flops = W.conv_bn_relu_dag(L, B), L.flops(B)
         if not a.bn:
             cfg.block_n = 256 if L.f >= 256 else (128 if L.f >= 128 else 64)
-    if a.trace:
+    if a.trace or a.gap:
         os.environ["TMB_TRACE"] = "1"
     plan = Plan(dag, cfg)
     ex = plan.bind(ins, outs)
+    if a.gap:
+        import numpy as np
+        from paper_2210_09603_b200 import Graph
+        exs = [ex] + [plan.bind(ins, outs) for _ in range(3)]
+        g = Graph(exs)
+        for _ in range(3):
+            g.launch()
+        torch.cuda.synchronize()
+        prev = None
+        for j, e in enumerate(exs):
+            tr = e.trace(0)
+            st, su, en = (tr[:, 0, k].astype(np.int64) for k in (7, 14, 15))
+            dl = tr[:, 1, 15].astype(np.int64)
+            if j == len(exs) - 1:
+                arr = tr[:, 2:15, 15].astype(np.int64)  # per-warp arrival at the final barrier
+                print("  warp arrival at final barrier, CTA 0 (us after entry):",
+                      " ".join(f"{(x - st[0]) / 1e3:.2f}" for x in arr[0]))
+                print(f"  CTA 0: exit {(en[0] - st[0]) / 1e3:.2f}, MMA warp past barrier "
+                      f"{(tr[0, 1, 14] - st[0]) / 1e3:.2f}, dealloc done {(dl[0] - st[0]) / 1e3:.2f}")
+            line = (f"launch {j}: entry span {(st.max() - st.min()) / 1e3:.2f} us, life {(en.max() - st.min()) / 1e3:.2f} us,"
+                    f" dealloc done +{(dl.max() - en.max()) / 1e3:.2f} us after the last exit")
+            if prev is not None:
+                line += f"  | gap from previous last exit to first entry {(st.min() - prev) / 1e3:.2f} us"
+            prev = en.max()
+            print(line)
     for _ in range(3):
         ex.launch()
     torch.cuda.synchronize()
+    # a CUDA graph of `iters` back-to-back launches: device time without host launch cost
+    from paper_2210_09603_b200 import Graph
+    g = Graph([ex] * a.iters)
+    g.launch()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(a.iters):
-        ex.launch()
+    g.launch()
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.iters
@@ -95,12 +125,13 @@ def main():
         ex.launch()
         torch.cuda.synchronize()
         tr = ex.trace(0)
-        names = ["prodF", "prodL", "mmaF", "mmaL", "epiRdy", "epiAcc", "epiDone", "-", "ldS", "ldW", "ep0", "st0",
-                 "ep1", "st1"]
+        names = ["prodF", "prodL", "mmaF", "mmaL", "epiRdy", "epiAcc", "epiDone", "-", "ld0", "ldback", "bufok",
+                 "staged", "stored", "staged1", "-"]
         for cta in (0, 1, tr.shape[0] - 1):
             print(f"CTA {cta} (cycles):")
             for i in range(64):
-                row = tr[cta, i, :14]
+                row = tr[cta, i, :15].copy()
+                row[7] = 0
                 if not row.any():
                     continue
                 print(f"  tile {i:2d} " + " ".join(f"{n}={v:7d}" for n, v in zip(names, row)))
@@ -108,6 +139,10 @@ def main():
         span = done.max(axis=1)
         mma = np.where(tr[:, :, 3] > 0, tr[:, :, 3] - tr[:, :, 2], 0)
         epi = np.where(tr[:, :, 6] > 0, tr[:, :, 6] - tr[:, :, 5], 0)
+        st, su, en = (tr[:, 0, j].astype(np.int64) for j in (7, 14, 15))
+        print(f"globaltimer: CTA entry spread {(st.max() - st.min()) / 1e3:.2f} us; setup median "
+              f"{np.median(su - st) / 1e3:.2f} us; CTA life median {np.median(en - st) / 1e3:.2f} us, "
+              f"first entry -> last exit {(en.max() - st.min()) / 1e3:.2f} us")
         print(f"CTA span cycles: min {span.min()} median {np.median(span):.0f} max {span.max()}; "
               f"per-tile MMA issue span mean {mma[mma > 0].mean():.0f}; epilogue mean {epi[epi > 0].mean():.0f}")
     print(json.dumps({"case": a.case, "ms": ms, "tflops": flops / ms / 1e9, "launches": ex.num_launches,

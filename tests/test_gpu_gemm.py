@@ -260,3 +260,30 @@ def test_ffn_chain():
     # absolute error, so bound it relative to the output scale.
     want = port.ffn(x, w1, b1, w2, b2)
     assert np.abs(got["O"] - want).max() / np.abs(want).max() <= 1e-2
+
+
+def test_graph_replay_matches_eager_and_times_each_exec():
+    """tm_graph: a captured sequence of execs (including a split-K one, whose
+    counters must self-reset across replays) reproduces the eager results, and a
+    timed graph reports one positive duration per exec."""
+    import torch
+    from paper_2210_09603_b200 import Graph, Plan
+    m, n, k = 384, 256, 320
+    a, b, bias = _matmul_case(m, n, k, True, 41)
+    dag = matmul_epilogue_dag(m, n, k, DType.I32)
+    ins = [dev(a), dev(b), dev(bias, "f32")]
+    outs = [torch.empty((m, n), dtype=torch.float32, device="cuda") for _ in range(2)]
+    execs = [Plan(dag, ScheduleConfig(split_k=sk)).bind(ins, [o]) for sk, o in zip((1, 3), outs)]
+    want = port.matmul_bias_relu(a, b, bias)
+    for timed in (False, True):
+        g = Graph(execs, timed=timed)
+        for _ in range(3):
+            for o in outs:
+                o.fill_(float("nan"))
+            g.launch()
+            torch.cuda.synchronize()
+            for o in outs:
+                assert np.array_equal(o.cpu().numpy(), want)
+        if timed:
+            ms = g.exec_ms()
+            assert len(ms) == 2 and all(t > 0 for t in ms)
