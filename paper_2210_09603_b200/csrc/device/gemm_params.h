@@ -79,9 +79,12 @@ enum LoaderKind : int32_t {
   LD_IM2COL_GATHER = 3, // predicated im2col gather from any-strided X (A only)
   LD_IM2COL_TMA = 4,    // TMA im2col mode on channels-last X (A only)
   LD_FILTER_GATHER = 5, // conv filter W[F,C,Kh,Kw] with any strides (B only)
-  LD_IM2COL_TMA8 = 6    // small-C conv (C <= 8, 16-byte padded channels-last X): one
+  LD_IM2COL_TMA8 = 6,   // small-C conv (C <= 8, 16-byte padded channels-last X): one
                         // TMA im2col box {8 ch x 128 px} per tap, 8 taps per k-block,
                         // no-swizzle K-major smem layout; K order (tap, c < 8)
+  LD_IM2COL_G8 = 7      // same layout and K order as LD_IM2COL_TMA8, gathered by the
+                        // 128 loader threads: one 16-byte load per (pixel, tap), the
+                        // channels >= C masked to zero (no per-box TMA cost: 49 taps)
 };
 
 // A strided operand: element (row, k, batch) at

@@ -187,6 +187,58 @@ __device__ __forceinline__ void gather_row_im2col(uint8_t* tile, int r, const Co
   }
 }
 
+// Small-C im2col gather of one tile row (one output pixel) for k-block kb:
+// BK/8 taps of one 16-byte pixel each (C <= 8 channels stored 16-byte padded,
+// channels-last), as cp.async copies into the no-swizzle layout of
+// LD_IM2COL_TMA8 ([tap][pixel][16 B]).  Asynchronous, so a loader thread runs
+// ahead over the whole ring instead of waiting for each stage's loads.
+// Padding taps and channels >= C are zero, as the reference Col node's select
+// (compute_ir.cpp:539-553).
+struct G8Row {
+  int64_t base;  // pixel index of (img, 0, 0) in 16-byte units
+  int bh, bw;    // top-left input coordinate of the output pixel's window
+  bool ok;
+};
+
+// per tile: this thread's output pixel (tile row r)
+__device__ __forceinline__ G8Row g8_row(const ConvGeom& g, int64_t pix, int64_t M) {
+  G8Row rw;
+  rw.ok = pix < M;
+  const int hw = g.ho * g.wo;
+  const int img = rw.ok ? static_cast<int>(pix / hw) : 0;
+  const int rem = rw.ok ? static_cast<int>(pix - static_cast<int64_t>(img) * hw) : 0;
+  const int oh = rem / g.wo, ow = rem - (rem / g.wo) * g.wo;
+  rw.bh = oh * g.stride - g.pad;
+  rw.bw = ow * g.stride - g.pad;
+  rw.base = static_cast<int64_t>(img) * (g.sx[0] >> 3);
+  return rw;
+}
+
+template <int BK>
+__device__ __forceinline__ void gather_g8(uint8_t* tile, int r, const ConvGeom& g, const G8Row& rw, int kb) {
+  static_assert(BK == 64, "8 taps of 8 channels per k-block");
+  const uint4* x = reinterpret_cast<const uint4*>(g.x);  // one pixel = 16 B (pixel stride 8 elements)
+  const int64_t s_h = g.sx[2] >> 3, s_w = g.sx[3] >> 3;
+  const uint32_t nb = 2u * static_cast<uint32_t>(g.c);  // bytes of the c < C channels of a pixel
+  const int taps = g.kh * g.kw;
+  int tap = kb * 8;
+  int fh = tap / g.kw, fw = tap - fh * g.kw;
+  uint8_t* dst = tile + (r >> 3) * 1024 + (r & 7) * 16;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int ih = rw.bh + fh, iw = rw.bw + fw;
+    const bool ok = rw.ok && tap < taps && static_cast<unsigned>(ih) < static_cast<unsigned>(g.h) &&
+                    static_cast<unsigned>(iw) < static_cast<unsigned>(g.w);
+    // tap-adjacent no-swizzle layout: core matrix (8 rows x 16 B) of (row group, tap)
+    // at (r / 8) * 1024 + j * 128 (LBO = 128 along K, SBO = 1024 along M);
+    // padding taps copy 0 bytes (all zero), channels >= C are zero-filled
+    ptx::cp_async16_ca(dst + j * 128, ok ? static_cast<const void*>(x + rw.base + ih * s_h + iw * s_w) : g.x,
+                       ok ? nb : 0u);
+    ++tap;
+    if (++fw == g.kw) { fw = 0; ++fh; }
+  }
+}
+
 // Filter gather of one tile row (= one output channel f) of Wf (the flatten
 // node, compute_ir.cpp:558-569), any strides of W, either K order.
 template <bool TF32, int BK>
@@ -618,7 +670,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     if (a_tma) ptx::tma_prefetch_desc(&tmA);
     if (b_tma) ptx::tma_prefetch_desc(&tmB);
     for (int s = 0; s < STAGES; ++s) {
-      ptx::mbar_init(&full[s], all_tma ? 1 : 128);
+      ptx::mbar_init(&full[s], all_tma ? 2 : 128);  // all-TMA: the A and B issuing warps
       ptx::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -647,61 +699,141 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     // diagnostics: setup + teardown only
   } else if (warp < 4) {
     // ===================== loaders (prologue splice) =====================
+    // All-TMA operands: lane 0 of each of the 4 loader warps issues every 4th
+    // ring slot (slot q -> warp q % 4).  TMA copies issued by one thread are
+    // serviced one after another (~600 clk per box, nearly size-independent,
+    // measured by scripts/tmabench.cu), so a single issuing thread caps a CTA
+    // near 30 B/clk; four issuing warps run four copy streams in parallel.
     const int t = threadIdx.x;  // 0..127
-    if (all_tma && t != 0) {
-      // idle: single-thread TMA producer
+    const uint32_t lw = static_cast<uint32_t>(t >> 5);
+    if (all_tma && (t & 31) != 0) {
+      // idle lanes
     } else {
       int stage = 0;
       uint32_t phase = 0;
+      uint32_t q = 0;  // ring slot sequence number
       int b, ks, tm_, tn;
       bool valid;
       for (uint32_t i = 0; detail::next_tile<CG>(p, i, b, ks, tm_, tn, valid); ++i) {
         if (!valid) continue;
         // this CTA's rows of A and columns of B (half of each tile's B when CG == 2)
         const int m0 = tm_ * kTileM + rank * kBM, n0 = tn * BN + rank * (BN / CG);
-        for (int kb0 = ks * p.kb_per_split, kb = kb0, kb_end = min(p.num_kb, kb0 + p.kb_per_split); kb < kb_end; ++kb) {
+        detail::G8Row g8{};
+        if (GENERIC && p.a_loader == LD_IM2COL_G8) g8 = detail::g8_row(p.conv, m0 + t, p.M);
+        for (int kb0 = ks * p.kb_per_split, kb = kb0, kb_end = min(p.num_kb, kb0 + p.kb_per_split); kb < kb_end; ++kb, ++q) {
+          // every loader waits for every slot (a warp may not run more than one
+          // ring phase ahead, or the parity wait would alias); only the owner issues
           if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&empty[stage], phase ^ 1u);
           else ptx::mbar_wait(&empty[stage], phase ^ 1u);
-          if (kb == kb0 && t == 0) detail::trace(p, i, TR_PROD_FIRST, t0);
-          if (kb == kb_end - 1 && t == 0) detail::trace(p, i, TR_PROD_LAST, t0);
           uint8_t* a_tile = smA + stage * Cfg::A_BYTES;
           uint8_t* b_tile = smB + stage * Cfg::B_BYTES;
           const int k0 = kb * BK;
-          if constexpr (CG == 2) {
-            // both CTAs' TMA bytes complete on the leader's full barrier
-            const uint32_t lead_full = ptx::mapa_shared(ptx::smem_u32(&full[stage]), 0);
-            if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], CG * Cfg::STAGE_BYTES);
-            if (p.a_loader == LD_TMA_K) {
-              ptx::tma_load_3d_2sm(a_tile, &tmA, lead_full, k0, m0, b);
-            } else {
-              const int cblocks = p.conv.c / BK;
-              const int tap = kb / cblocks, cb = kb % cblocks;
-              const int fh = tap / p.conv.kw, fw = tap % p.conv.kw;
-              const int hw = p.conv.ho * p.conv.wo;
-              const int img = m0 / hw, rem = m0 % hw;
-              const int oh = rem / p.conv.wo, ow = rem % p.conv.wo;
-              ptx::tma_load_im2col_4d_2sm(a_tile, &tmA, lead_full, cb * BK, ow * p.conv.stride - p.conv.pad,
-                                          oh * p.conv.stride - p.conv.pad, img, static_cast<uint16_t>(fw),
-                                          static_cast<uint16_t>(fh));
-            }
-            if (p.b_loader == LD_TMA_K) {
-              ptx::tma_load_3d_2sm(b_tile, &tmB, lead_full, k0, n0, b);
-            } else {
+          if (all_tma) {
+            // slot q: A from warp 2q mod 4, B from warp 2q+1 mod 4 (full barrier count 2)
+            const bool do_a = ((2u * q) & 3u) == lw, do_b = ((2u * q + 1u) & 3u) == lw;
+            if (p.dbg == 3) {  // diagnostics: no copies (MMA on stale smem) -> MMA + epilogue floor
+              if (do_a || do_b) {
+                if constexpr (CG == 2) {
+                  if (rank == 0) ptx::mbar_arrive(&full[stage]);
+                } else {
+                  ptx::mbar_arrive(&full[stage]);
+                }
+              }
+            } else if (do_a || do_b) {
+              if (kb == kb0) detail::trace(p, i, TR_PROD_FIRST, t0);
+              if (kb == kb_end - 1) detail::trace(p, i, TR_PROD_LAST, t0);
+              if constexpr (CG == 2) {
+                // both CTAs' TMA bytes complete on the leader's full barrier
+                const uint32_t lead_full = ptx::mapa_shared(ptx::smem_u32(&full[stage]), 0);
+                if (do_a) {
+                  if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], CG * Cfg::A_BYTES);
+                  if (p.a_loader == LD_TMA_K) {
+                    ptx::tma_load_3d_2sm(a_tile, &tmA, lead_full, k0, m0, b);
+                  } else {
+                    const int cblocks = p.conv.c / BK;
+                    const int tap = kb / cblocks, cb = kb % cblocks;
+                    const int fh = tap / p.conv.kw, fw = tap % p.conv.kw;
+                    const int hw = p.conv.ho * p.conv.wo;
+                    const int img = m0 / hw, rem = m0 % hw;
+                    const int oh = rem / p.conv.wo, ow = rem % p.conv.wo;
+                    ptx::tma_load_im2col_4d_2sm(a_tile, &tmA, lead_full, cb * BK, ow * p.conv.stride - p.conv.pad,
+                                                oh * p.conv.stride - p.conv.pad, img, static_cast<uint16_t>(fw),
+                                                static_cast<uint16_t>(fh));
+                  }
+                }
+                if (do_b) {
+                  if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], CG * Cfg::B_BYTES);
+                  if (p.b_loader == LD_TMA_K) {
+                    ptx::tma_load_3d_2sm(b_tile, &tmB, lead_full, k0, n0, b);
+                  } else {
 #pragma unroll 1
-              for (int j = 0; j < BN / CG / 64; ++j)
-                ptx::tma_load_3d_2sm(b_tile + j * (64 * kRowBytes), &tmB, lead_full, n0 + 64 * j, k0, b);
+                    for (int j = 0; j < BN / CG / 64; ++j)
+                      ptx::tma_load_3d_2sm(b_tile + j * (64 * kRowBytes), &tmB, lead_full, n0 + 64 * j, k0, b);
+                  }
+                }
+              } else {
+                if (do_a) {
+                  ptx::mbar_arrive_expect_tx(&full[stage], Cfg::A_BYTES);
+                  if (p.a_loader == LD_TMA_K) {
+                    ptx::tma_load_3d(a_tile, &tmA, &full[stage], k0, m0, b);
+                  } else if (p.a_loader == LD_IM2COL_TMA) {
+                    // K block = (tap, channel block); rows = 128 consecutive output pixels.
+                    const int cblocks = p.conv.c / BK;
+                    const int tap = kb / cblocks, cb = kb % cblocks;
+                    const int fh = tap / p.conv.kw, fw = tap % p.conv.kw;
+                    const int hw = p.conv.ho * p.conv.wo;
+                    const int img = m0 / hw, rem = m0 % hw;
+                    const int oh = rem / p.conv.wo, ow = rem % p.conv.wo;
+                    ptx::tma_load_im2col_4d(a_tile, &tmA, &full[stage], cb * BK, ow * p.conv.stride - p.conv.pad,
+                                            oh * p.conv.stride - p.conv.pad, img, static_cast<uint16_t>(fw),
+                                            static_cast<uint16_t>(fh));
+                  } else {  // LD_IM2COL_TMA8
+                    // 8 taps per k-block, one {8 ch x 128 px} box each (2 KB, dense rows of
+                    // 16 B = one core-matrix column); taps past the window repeat the last
+                    // one (the filter is zero there, and the data is finite)
+                    const int hw = p.conv.ho * p.conv.wo;
+                    const int img = m0 / hw, rem = m0 % hw;
+                    const int oh = rem / p.conv.wo, ow = rem % p.conv.wo;
+                    const int taps = p.conv.kh * p.conv.kw;
+#pragma unroll 1
+                    for (int j = 0; j < BK / 8; ++j) {
+                      const int tap = min(kb * (BK / 8) + j, taps - 1);
+                      ptx::tma_load_im2col_4d(a_tile + j * 2048, &tmA, &full[stage], 0,
+                                              ow * p.conv.stride - p.conv.pad, oh * p.conv.stride - p.conv.pad, img,
+                                              static_cast<uint16_t>(tap % p.conv.kw),
+                                              static_cast<uint16_t>(tap / p.conv.kw));
+                    }
+                  }
+                }
+                if (do_b) {
+                  ptx::mbar_arrive_expect_tx(&full[stage], Cfg::B_BYTES);
+                  if (p.b_loader == LD_TMA_K) {
+                    ptx::tma_load_3d(b_tile, &tmB, &full[stage], k0, n0, b);
+                  } else {
+#pragma unroll 1
+                    for (int j = 0; j < BN / 64; ++j)
+                      ptx::tma_load_3d(b_tile + j * (64 * kRowBytes), &tmB, &full[stage], n0 + 64 * j, k0, b);
+                  }
+                }
+              }
             }
             if (++stage == STAGES) { stage = 0; phase ^= 1u; }
             continue;
           }
-          if (all_tma) {
-            ptx::mbar_arrive_expect_tx(&full[stage], Cfg::STAGE_BYTES);
-          } else if (t == 0) {
+          // ---- mixed / gather mode (GENERIC): lane 0 of warp q % 4 issues the slot's
+          // TMA operand (TMA copies from one thread are serviced serially), all 128 gather
+          const bool issuer = t == static_cast<int>((q & 3u) << 5);
+          if (kb == kb0 && issuer) detail::trace(p, i, TR_PROD_FIRST, t0);
+          if (kb == kb_end - 1 && issuer) detail::trace(p, i, TR_PROD_LAST, t0);
+          if constexpr (CG == 2) {
+            __trap();  // the CTA-pair form is instantiated for TMA operands only
+          }
+          if (issuer) {
             // mixed mode: announce the TMA bytes now, arrive after the gather
             const uint32_t tx = (a_tma ? Cfg::A_BYTES : 0) + (b_tma ? Cfg::B_BYTES : 0);
             if (tx) ptx::mbar_expect_tx(&full[stage], tx);
           }
-          if (t == 0) {
+          if (issuer) {
             if (p.a_loader == LD_TMA_K) {
               ptx::tma_load_3d(a_tile, &tmA, &full[stage], k0, m0, b);
             } else if (p.a_loader == LD_IM2COL_TMA) {
@@ -748,8 +880,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
               const bool ok = row < p.M;
               if (p.a_loader == LD_GATHER)
                 detail::gather_row_strided<TF32, BK>(a_tile, t, p.a, row, ok, b, k0, p.K);
-              else
+              else if (p.a_loader == LD_IM2COL_G8) {
+                if constexpr (!TF32) {
+                  if (p.dbg != 3) detail::gather_g8<BK>(a_tile, t, p.conv, g8, kb);  // async, arrives below
+                }
+              } else {
                 detail::gather_row_im2col<TF32, BK>(a_tile, t, p.conv, row, ok, k0, p.K);
+              }
             }
             if (!b_tma) {
 #pragma unroll 1
@@ -762,8 +899,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
                   detail::gather_row_filter<TF32, BK>(b_tile, r, p.conv, row, ok, k0, p.K);
               }
             }
-            ptx::fence_proxy_async_smem();
-            ptx::mbar_arrive(&full[stage]);
+            if (p.a_loader == LD_IM2COL_G8 && b_tma) {
+              ptx::cp_async_arrive_noinc(&full[stage]);  // when this thread's copies land
+            } else {
+              if (p.a_loader == LD_IM2COL_G8) asm volatile("cp.async.wait_all;" ::: "memory");
+              ptx::fence_proxy_async_smem();
+              ptx::mbar_arrive(&full[stage]);
+            }
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1u; }
         }
@@ -1036,13 +1178,29 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     if (p.out_tma && lane == 0) ptx::bulk_wait<0>();  // all output tiles written before exit
   } else {
-    // ===================== MMA issuer (single thread) =====================
-    if (lane == 0 && rank == 0) {
+    // ===================== MMA issuer =====================
+    // The whole warp walks the ring (warp-uniform control flow); one elected
+    // lane issues each k-block's tcgen05.mma group and its commit.  Descriptors
+    // are built once: per stage / per K16 step they only move the start address
+    // field (addr >> 4 in bits [0,14)), so the issue loop is adds on uniform
+    // registers.
+    if (rank == 0) {
       const bool b_mn = p.b_loader == LD_TMA_MN;
       const bool a_noswz = p.a_loader == LD_IM2COL_TMA8;
+      const bool a_g8 = p.a_loader == LD_IM2COL_G8;
       const uint32_t idesc = ptx::make_idesc(kTileM, BN, TF32 ? 2u : 1u, false, b_mn);
       const uint32_t mn_lbo = p.mn_lbo_sbo_swap ? 1024u : 64u * kRowBytes;
       const uint32_t mn_sbo = p.mn_lbo_sbo_swap ? 64u * kRowBytes : 1024u;
+      const uint32_t a0 = ptx::smem_u32(smA), b0 = ptx::smem_u32(smB);
+      // 2 taps (2 x 16 B chunks of 2 KB boxes) per K16 for the C<=8 im2col layout
+      // G8: taps adjacent (LBO 128 B along K, SBO 1024 B per 8 rows), 2 taps per K16
+      const uint64_t adesc0 = a_noswz ? ptx::smem_desc_noswz(a0, 2048, 128)
+                                      : a_g8 ? ptx::smem_desc_noswz(a0, 128, 1024) : ptx::smem_desc_sw128(a0, 16, 1024);
+      const uint64_t bdesc0 = b_mn ? ptx::smem_desc_sw128(b0, mn_lbo, mn_sbo) : ptx::smem_desc_sw128(b0, 16, 1024);
+      const uint32_t a_kstep = a_noswz ? (2u * 2048u) >> 4
+                                       : a_g8 ? (2u * 128u) >> 4 : static_cast<uint32_t>(Cfg::KSTEP * Cfg::kElem) >> 4;
+      const uint32_t b_kstep = b_mn ? static_cast<uint32_t>(Cfg::KSTEP * kRowBytes) >> 4
+                                    : static_cast<uint32_t>(Cfg::KSTEP * Cfg::kElem) >> 4;
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -1058,35 +1216,38 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         for (int kb0 = ks * p.kb_per_split, kb = kb0, kb_end = min(p.num_kb, kb0 + p.kb_per_split); kb < kb_end; ++kb) {
           if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&full[stage], phase);
           else ptx::mbar_wait(&full[stage], phase);
+          if (GENERIC && !all_tma) ptx::fence_proxy_async_smem();  // cp.async (generic proxy) -> tcgen05.mma
           ptx::tc_fence_after();
-          if (kb == kb0) detail::trace(p, i, TR_MMA_FIRST, t0);
-          const uint32_t a_addr = ptx::smem_u32(smA + stage * Cfg::A_BYTES);
-          const uint32_t b_addr = ptx::smem_u32(smB + stage * Cfg::B_BYTES);
+          if (kb == kb0 && lane == 0) detail::trace(p, i, TR_MMA_FIRST, t0);
+          const uint64_t ad = adesc0 + static_cast<uint64_t>((stage * Cfg::A_BYTES) >> 4);
+          const uint64_t bd = bdesc0 + static_cast<uint64_t>((stage * Cfg::B_BYTES) >> 4);
+          if (ptx::elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < Cfg::NSTEP; ++kk) {
-            const uint64_t adesc =
-                a_noswz ? ptx::smem_desc_noswz(a_addr + kk * 2 * 2048, 2048, 128)  // 2 taps (2 x 16 B chunks) per K16
-                        : ptx::smem_desc_sw128(a_addr + kk * Cfg::KSTEP * Cfg::kElem, 16, 1024);
-            const uint64_t bdesc =
-                b_mn ? ptx::smem_desc_sw128(b_addr + kk * Cfg::KSTEP * kRowBytes, mn_lbo, mn_sbo)
-                     : ptx::smem_desc_sw128(b_addr + kk * Cfg::KSTEP * Cfg::kElem, 16, 1024);
-            const uint32_t accum = (kb != kb0 || kk != 0);
-            if constexpr (CG == 2) {
-              if (TF32) ptx::mma_tf32_2sm(d_tmem, adesc, bdesc, idesc, accum);
-              else ptx::mma_f16_2sm(d_tmem, adesc, bdesc, idesc, accum);
-            } else {
-              if (TF32) ptx::mma_tf32(d_tmem, adesc, bdesc, idesc, accum);
-              else ptx::mma_f16(d_tmem, adesc, bdesc, idesc, accum);
+            for (int kk = 0; kk < Cfg::NSTEP; ++kk) {
+              const uint64_t adesc = ad + static_cast<uint64_t>(kk * a_kstep);
+              const uint64_t bdesc = bd + static_cast<uint64_t>(kk * b_kstep);
+              const uint32_t accum = (kb != kb0 || kk != 0);
+              if constexpr (CG == 2) {
+                if (TF32) ptx::mma_tf32_2sm(d_tmem, adesc, bdesc, idesc, accum);
+                else ptx::mma_f16_2sm(d_tmem, adesc, bdesc, idesc, accum);
+              } else {
+                if (TF32) ptx::mma_tf32(d_tmem, adesc, bdesc, idesc, accum);
+                else ptx::mma_f16(d_tmem, adesc, bdesc, idesc, accum);
+              }
             }
+            // frees this ring slot (in both CTAs of the pair)
+            if constexpr (CG == 2) ptx::mma_commit_2sm(&empty[stage], 0x3);
+            else ptx::mma_commit(&empty[stage]);
           }
-          // frees this ring slot in both CTAs of the pair
-          if constexpr (CG == 2) ptx::mma_commit_2sm(&empty[stage], 0x3);
-          else ptx::mma_commit(&empty[stage]);
+          __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1u; }
         }
-        if constexpr (CG == 2) ptx::mma_commit_2sm(&tfull[acc], 0x3);
-        else ptx::mma_commit(&tfull[acc]);
-        detail::trace(p, i, TR_MMA_LAST, t0);
+        if (ptx::elect_one()) {
+          if constexpr (CG == 2) ptx::mma_commit_2sm(&tfull[acc], 0x3);
+          else ptx::mma_commit(&tfull[acc]);
+        }
+        __syncwarp();
+        if (lane == 0) detail::trace(p, i, TR_MMA_LAST, t0);
         if (++acc == 2) { acc = 0; acc_phase ^= 1u; }
       }
     }

@@ -824,14 +824,12 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
                         sp.b.kind == OperandPlan::ConvFilter;
       g.korder = (im2col_tma || tma8) ? 1 : 0;
       g.cpad = tma8 ? 8 : static_cast<int32_t>(c.c);
-      p.a_loader = im2col_tma ? LD_IM2COL_TMA : tma8 ? LD_IM2COL_TMA8 : LD_IM2COL_GATHER;
+      // small C: 16-byte-per-(pixel, tap) LSU gather (LD_IM2COL_G8) -- a TMA box per
+      // tap (LD_IM2COL_TMA8) costs ~600 clk of TMA issue each, 49 of them per tile
+      p.a_loader = im2col_tma ? LD_IM2COL_TMA : tma8 ? LD_IM2COL_G8 : LD_IM2COL_GATHER;
       if (tma8) {
         p.K = static_cast<int32_t>(c.kh * c.kw * 8);  // K order (tap, 8 channels)
         p.num_kb = (p.K + BK - 1) / BK;
-        const uint64_t dims[4] = {(uint64_t)c.c, (uint64_t)c.w, (uint64_t)c.h, (uint64_t)c.n};
-        const uint64_t strides[3] = {16, (uint64_t)x.stride[2] * 2, (uint64_t)x.stride[0] * 2};
-        make_tma_im2col(k.tma_a, x.data, x.dtype, dims, strides, static_cast<int>(c.pad),
-                        static_cast<int>(c.pad - (c.kh - 1)), static_cast<int>(c.stride), 8, 128, false);
       }
       if (im2col_tma) {
         const uint64_t dims[4] = {(uint64_t)c.c, (uint64_t)c.w, (uint64_t)c.h, (uint64_t)c.n};
@@ -928,6 +926,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
     if (k.simt) {
       // fp32 CUDA-core kernel (simt_fp32.cu): 128x128 tiles, strided predicated loads
       if (p.a_loader == LD_IM2COL_GATHER || p.a_loader == LD_IM2COL_TMA || p.a_loader == LD_IM2COL_TMA8 ||
+          p.a_loader == LD_IM2COL_G8 ||
           p.b_loader == LD_FILTER_GATHER || sp.b.kind == OperandPlan::ConvFilter)
         fail("math=fp32_simt supports matrix operands only (conv im2col is not supported on this path)");
       k.bn = 128;

@@ -203,9 +203,10 @@ def test_conv_bn_relu_exact(geom, layout, bm):
 
 @pytest.mark.parametrize("geom", [(2, 3, 20, 20, 64, 7, 7, 2, 3), (1, 3, 17, 19, 32, 3, 3, 1, 1),
                                   (2, 4, 9, 9, 16, 5, 5, 2, 2)])
-def test_conv_small_channel_tma8_exact(geom):
-    """conv1-style C <= 8 on 16-byte padded channels-last input: one TMA im2col box per
-    tap (LD_IM2COL_TMA8, no-swizzle UMMA layout); pad channels are NaN in memory."""
+def test_conv_small_channel_g8_exact(geom):
+    """conv1-style C <= 8 on 16-byte padded channels-last input: one 16-byte gather per
+    (pixel, tap) (LD_IM2COL_G8, no-swizzle UMMA layout); pad channels are NaN in memory
+    and must be masked, padding taps zero (compute_ir.cpp:539-553)."""
     n, c, h, w, f, kh, kw, s, p = geom
     rng = port.Rng(6)
     x = rng.tensor((n, c, h, w), True)
@@ -218,7 +219,7 @@ def test_conv_small_channel_tma8_exact(geom):
     xs = dev(x, layout="cl8")
     out = torch.empty((n, f, ho, wo), dtype=torch.float32, device="cuda")
     ex = Plan(dag).bind([xs, dev(wt, layout="cl"), dev(scale, "f32"), dev(shift, "f32")], [out])
-    assert ex.kernel_info(0)["a_loader"] == 6  # LD_IM2COL_TMA8
+    assert ex.kernel_info(0)["a_loader"] == 7  # LD_IM2COL_G8
     ex.launch()
     torch.cuda.synchronize()
     assert np.array_equal(out.cpu().numpy().astype(np.float64), port.conv_bn_relu(x, wt, scale, shift, s, p))
