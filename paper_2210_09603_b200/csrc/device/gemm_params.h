@@ -59,7 +59,12 @@ constexpr int kTraceEvents = 16;  // 0-7 role events (TraceEv); tile 0: 14/15 = 
 // 32 rows x out_stage_row_bytes (a 64- or 128-byte swizzled row segment per
 // lane), written to global memory by one TMA store per column group.  64-byte
 // rows for BN = 256 single-CTA tiles, whose pipeline needs the shared memory.
-constexpr int out_stage_row_bytes(int bn, int cg) { return (bn == 256 && cg == 1) ? 64 : 128; }
+// The two epilogue warp groups split every tile's columns in halves (compact
+// kernel), so BN/2 must be a whole number of store groups: 64-byte rows
+// (32 bf16 columns) for BN = 64 and 192.
+constexpr int out_stage_row_bytes(int bn, int cg) {
+  return ((bn == 256 && cg == 1) || bn == 64 || bn == 192) ? 64 : 128;
+}
 // trace events per tile
 enum TraceEv : int32_t {
   TR_PROD_FIRST = 0,  // producer: first k-block slot acquired

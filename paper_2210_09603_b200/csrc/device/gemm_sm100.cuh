@@ -31,6 +31,18 @@ constexpr int kRowBytes = 128;    // one swizzle-128B row of K
 constexpr int kEpiWarps = 8;       // epilogue warps (2 groups x 4 TMEM lane groups)
 constexpr int kNumThreads = 32 * (4 + kEpiWarps + 1);  // loaders + epilogue + MMA
 
+// Warp roles.  Generic kernel (13 warps): 0-3 loaders (128 gather threads),
+// 4-11 epilogue, 12 MMA.  Compact kernel (all-TMA operands, 12 warps = 384
+// threads, which raises the register budget from 128 to 168 per thread):
+// 0-2 TMA loaders, 3 MMA, 4-11 epilogue.  Epilogue warps stay 4-11 in both
+// (TMEM lane group = warp % 4).
+template <bool GENERIC>
+struct Roles {
+  static constexpr int kLoadWarps = GENERIC ? 4 : 3;
+  static constexpr int kMmaWarp = GENERIC ? 4 + kEpiWarps : 3;
+  static constexpr int kThreads = 32 * (GENERIC ? 4 + kEpiWarps + 1 : 4 + kEpiWarps);
+};
+
 // CG = CTAs per MMA (cta_group): 1, or 2 for the SM-pair form where the tile
 // is (2*128) x BN, each CTA stages its 128 rows of A and BN/2 rows of B, and
 // the pair leader issues tcgen05.mma.cta_group::2 over both CTAs' smem.
@@ -522,16 +534,38 @@ __device__ __forceinline__ void store_out(const GemmParams& p, const float (&v)[
 // (+ bf16 residual, prefetched one step ahead) -> bf16 pack -> swizzled smem
 // staging -> one TMA store per OUT_ROW-byte column group.  The accumulator is
 // handed back to the MMA right after the last TMEM load.
+// bf16x2 pack with ReLU folded into the conversion (one instruction per 2 outputs)
+__device__ __forceinline__ uint32_t pack_relu_bf16x2(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+
 template <int BN, int CG, int OUT_ROW, int ACT, bool RES>
 __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t taddr, const float* colbuf,
                                            uint8_t* obuf, int ncols, int32_t col_base, int32_t row0,
-                                           int32_t b, int lane, const uint4* res, uint64_t* tempty_bar,
-                                           long long* tr, long long t0) {
+                                           int32_t b, int lane, const uint4* res, uint64_t* tempty_bar) {
   constexpr int GC = OUT_ROW / 2;  // bf16 columns per TMA store group (32 or 64)
-  // optional fine timeline of the first two steps (tr != null: one warp, one tile)
-  auto tick = [&](int c, int ev) {
-    if (tr != nullptr && lane == 0 && (c == 0 || ev == 13)) tr[ev] = clock64() - t0;
+  auto release = [&]() {  // the MMA may reuse this accumulator buffer
+    ptx::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+      if constexpr (CG == 2) ptx::mbar_arrive_remote(ptx::mapa_shared(ptx::smem_u32(tempty_bar), 0));
+      else ptx::mbar_arrive(tempty_bar);
+    }
   };
+  if (ncols <= 0) {  // nothing of this column range is inside the output
+    release();
+    return;
+  }
+  // this lane's staged row: OUT_ROW bytes, 16-byte chunks XOR-swizzled as the TMA store expects
+  uint8_t* const orow = obuf + lane * OUT_ROW;
+  const int swz = OUT_ROW == 128 ? (lane & 7) : ((lane >> 1) & 3);
   uint4 rq[4];
   if constexpr (RES) {
 #pragma unroll
@@ -540,7 +574,6 @@ __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t tadd
 #pragma unroll 1
   for (int c = 0; c < ncols; c += 32) {
     uint32_t r[32];
-    tick(c, 8);
     ptx::tmem_ld32(taddr + c, r);
     uint4 rn[4];
     if constexpr (RES) {
@@ -550,20 +583,11 @@ __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t tadd
       }
     }
     ptx::tmem_wait_ld();
-    tick(c, 9);
-    if (c + 32 >= ncols) {  // last TMEM read of this tile: the MMA may reuse the buffer
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) {
-        if constexpr (CG == 2) ptx::mbar_arrive_remote(ptx::mapa_shared(ptx::smem_u32(tempty_bar), 0));
-        else ptx::mbar_arrive(tempty_bar);
-      }
-    }
+    if (c + 32 >= ncols) release();  // last TMEM read of this tile
     if (c % GC == 0) {  // the previous store from this buffer has read it
       if (lane == 0) ptx::bulk_wait_read<0>();
       __syncwarp();
     }
-    tick(c, 10);
     uint32_t w[16];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -571,6 +595,11 @@ __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t tadd
       const float4 tv = *reinterpret_cast<const float4*>(colbuf + BN + c + 4 * q);
       float x[4] = {fmaf(__uint_as_float(r[4 * q]), sv.x, tv.x), fmaf(__uint_as_float(r[4 * q + 1]), sv.y, tv.y),
                     fmaf(__uint_as_float(r[4 * q + 2]), sv.z, tv.z), fmaf(__uint_as_float(r[4 * q + 3]), sv.w, tv.w)};
+      if constexpr (ACT == 1 && !RES) {
+        w[2 * q] = pack_relu_bf16x2(x[0], x[1]);
+        w[2 * q + 1] = pack_relu_bf16x2(x[2], x[3]);
+        continue;
+      }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if constexpr (ACT == 1) x[j] = fmaxf(x[j], 0.f);
@@ -584,20 +613,13 @@ __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t tadd
         x[2] += __uint_as_float(w1 << 16);
         x[3] += __uint_as_float(w1 & 0xFFFF0000u);
       }
-      __nv_bfloat162 h0 = __floats2bfloat162_rn(x[0], x[1]);
-      __nv_bfloat162 h1 = __floats2bfloat162_rn(x[2], x[3]);
-      w[2 * q] = *reinterpret_cast<uint32_t*>(&h0);
-      w[2 * q + 1] = *reinterpret_cast<uint32_t*>(&h1);
+      w[2 * q] = pack_bf16x2(x[0], x[1]);
+      w[2 * q + 1] = pack_bf16x2(x[2], x[3]);
     }
-    const int j0 = (c % GC) / 8;  // 16-byte chunk of this lane's staged row
+    const int j0 = (c % GC) / 8;  // first 16-byte chunk of these 32 columns in the staged row
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      uint32_t a = static_cast<uint32_t>(lane * OUT_ROW + (j0 + k) * 16);
-      a ^= ((a >> 7) & (OUT_ROW == 128 ? 7u : 3u)) << 4;  // the TMA store's swizzle
-      *reinterpret_cast<uint4*>(obuf + a) = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
-    }
-    tick(c, 11);
-    if (c == 32) tick(c, 13);
+    for (int k = 0; k < 4; ++k)
+      *reinterpret_cast<uint4*>(orow + (((j0 + k) ^ swz) << 4)) = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
     if ((c + 32) % GC == 0 || c + 32 >= ncols) {
       ptx::fence_proxy_async_smem();
       __syncwarp();
@@ -606,7 +628,6 @@ __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t tadd
         ptx::bulk_commit();
       }
     }
-    tick(c, 12);
     if constexpr (RES) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) rq[q] = rn[q];
@@ -638,7 +659,7 @@ __device__ __forceinline__ bool next_tile(const GemmParams& p, uint32_t i, int& 
 }  // namespace detail
 
 template <int BN, int STAGES, bool TF32, int CG, bool GENERIC>
-__global__ void __launch_bounds__(kNumThreads, 1)
+__global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
     tm_gemm_kernel(const __grid_constant__ GemmParams p, const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmC) {
   using Cfg = GemmCfg<BN, STAGES, TF32, CG, GENERIC>;
@@ -675,11 +696,13 @@ __global__ void __launch_bounds__(kNumThreads, 1)
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
-      ptx::mbar_init(&tempty[a], 4 * CG);  // the group's 4 warps (of both CTAs) drained it
+      // drained by: the group's 4 warps, or all 8 when the groups split columns (of both CTAs)
+      ptx::mbar_init(&tempty[a], (!GENERIC && p.split_k == 1 ? 8 : 4) * CG);
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 4 + kEpiWarps) {
+  using R = Roles<GENERIC>;
+  if (warp == R::kMmaWarp) {
     if constexpr (CG == 2) ptx::tmem_alloc_2sm<Cfg::TMEM_COLS>(tmem_slot);
     else ptx::tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
   }
@@ -688,6 +711,12 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // Programmatic dependent launch: everything above (barrier init, TMEM
+  // allocation, descriptor prefetch) overlapped the previous kernel's tail;
+  // from here on this grid reads its inputs and writes its outputs, so wait
+  // for the previous grid, and let the next one start placing CTAs.
+  ptx::griddep_launch_dependents();
+  ptx::griddep_wait();
   const long long t0 = clock64();
   if (p.trace != nullptr && threadIdx.x == 0) {  // ns: kernel entry, setup done (tile 0's slots 7, 14)
     long long* tr0 = p.trace + static_cast<int64_t>(blockIdx.x) * kTraceTiles * kTraceEvents;
@@ -697,7 +726,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
 
   if (p.dbg == 1) {
     // diagnostics: setup + teardown only
-  } else if (warp < 4) {
+  } else if (warp < R::kLoadWarps) {
     // ===================== loaders (prologue splice) =====================
     // All-TMA operands: lane 0 of each of the 4 loader warps issues every 4th
     // ring slot (slot q -> warp q % 4).  TMA copies issued by one thread are
@@ -730,7 +759,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           const int k0 = kb * BK;
           if (all_tma) {
             // slot q: A from warp 2q mod 4, B from warp 2q+1 mod 4 (full barrier count 2)
-            const bool do_a = ((2u * q) & 3u) == lw, do_b = ((2u * q + 1u) & 3u) == lw;
+            const bool do_a = (2u * q) % R::kLoadWarps == lw, do_b = (2u * q + 1u) % R::kLoadWarps == lw;
             if (p.dbg == 3) {  // diagnostics: no copies (MMA on stale smem) -> MMA + epilogue floor
               if (do_a || do_b) {
                 if constexpr (CG == 2) {
@@ -911,7 +940,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         }
       }
     }
-  } else if (warp < 4 + kEpiWarps) {
+  } else if (warp >= 4 && warp < 4 + kEpiWarps) {
     // ===================== epilogue (epilogue splice) =====================
     // Two warp groups, one per TMEM accumulator buffer: group h drains the
     // CTA's tiles 1 mod 2 == h, so two tiles' epilogues overlap and each warp
@@ -982,19 +1011,46 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         ptx::bulk_commit();
       }
     };
-    auto release_acc = [&]() {
+    auto release_acc = [&](uint32_t buf) {
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) {
         // the (leader's) MMA may overwrite this accumulator once both CTAs drained it
-        if constexpr (CG == 2) ptx::mbar_arrive_remote(ptx::mapa_shared(ptx::smem_u32(&tempty[grp]), 0));
-        else ptx::mbar_arrive(&tempty[grp]);
+        if constexpr (CG == 2) ptx::mbar_arrive_remote(ptx::mapa_shared(ptx::smem_u32(&tempty[buf]), 0));
+        else ptx::mbar_arrive(&tempty[buf]);
       }
     };
     uint32_t nvalid = 0;
+    const bool colsplit = !GENERIC && p.split_k == 1;
+    uint32_t acc_phase2[2] = {0u, 0u};  // colsplit: per-buffer phase
+    // canonical S / T of columns gt and gt + 128 of tile column block tn_ (batch b_)
+    auto fetch_st = [&](int tn_, int b_, float (&s_v)[2], float (&t_v)[2]) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int64_t col = static_cast<int64_t>(tn_) * BN + gt + 128 * h;
+        const bool in = gt + 128 * h < BN && col < p.N;
+        s_v[h] = p.canon_s;
+        t_v[h] = p.canon_t;
+        if (p.canon_s_op >= 0 && in) {
+          const EpiOp& op = p.ops[p.canon_s_op];
+          s_v[h] = detail::load_side(op.ptr, detail::addr_rowpart(op.a, 0, b_) + col * op.a.s_col, op.dtype);
+        }
+        if (p.canon_t_op >= 0 && in) {
+          const EpiOp& op = p.ops[p.canon_t_op];
+          t_v[h] = detail::load_side(op.ptr, detail::addr_rowpart(op.a, 0, b_) + col * op.a.s_col, op.dtype);
+        }
+      }
+    };
+    float pf_s[2] = {0.f, 0.f}, pf_t[2] = {0.f, 0.f};
+    int pf_tn = -1, pf_b = -1;
     for (uint32_t i = 0; detail::next_tile<CG>(p, i, b, ks, tm_, tn, valid); ++i) {
       if (!valid) continue;
-      if ((nvalid++ & 1u) != static_cast<uint32_t>(grp)) continue;  // the other group's tile
+      // accumulator buffer = tile parity.  Compact kernel (no split-K): both groups
+      // drain every tile, group g the column half g (a tile's drain takes half as
+      // long, which is what the last tile of a CTA exposes); otherwise group g
+      // drains the tiles of parity g, full width.
+      const uint32_t abuf = nvalid++ & 1u;
+      if (!colsplit && abuf != static_cast<uint32_t>(grp)) continue;  // the other group's tile
       const int64_t n0 = static_cast<int64_t>(tn) * BN;
       const int tile_row0 = tm_ * kTileM + rank * kBM;
       const int row0 = tile_row0 + lg * 32;  // this warp's first row
@@ -1007,19 +1063,38 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       const bool restage = (staged_tn < 0 && (has_col || p.canon)) || (has_col && (tn != staged_tn || b != staged_b));
       if (restage) ptx::named_bar_sync(1 + grp, 128);  // the group's previous readers are done
       if (restage && p.canon) {  // S and T column vectors of the canonical epilogue
-        for (int c = gt; c < BN; c += 128) {
-          const bool in = n0 + c < p.N;
-          float sv = p.canon_s, tv = p.canon_t;
-          if (p.canon_s_op >= 0 && in) {
-            const EpiOp& op = p.ops[p.canon_s_op];
-            sv = detail::load_side(op.ptr, detail::addr_rowpart(op.a, 0, b) + (n0 + c) * op.a.s_col, op.dtype);
+        float s_v[2], t_v[2];
+        if (pf_tn == tn && pf_b == b) {  // prefetched while the previous tile drained
+          s_v[0] = pf_s[0]; s_v[1] = pf_s[1]; t_v[0] = pf_t[0]; t_v[1] = pf_t[1];
+        } else {
+          fetch_st(tn, b, s_v, t_v);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = gt + 128 * h;
+          if (c < BN) {
+            colbuf[c] = s_v[h];
+            colbuf[BN + c] = t_v[h];
           }
-          if (p.canon_t_op >= 0 && in) {
-            const EpiOp& op = p.ops[p.canon_t_op];
-            tv = detail::load_side(op.ptr, detail::addr_rowpart(op.a, 0, b) + (n0 + c) * op.a.s_col, op.dtype);
+        }
+      }
+      if (p.canon && has_col) {
+        // look ahead to this group's next tile; if its columns differ, start
+        // loading its S / T now so the loads overlap this tile's drain
+        pf_tn = -1;
+        int nb_, nks_, ntm_, ntn_;
+        bool nv_;
+        uint32_t need = colsplit ? 1u : 2u;
+        for (uint32_t j = i + 1; detail::next_tile<CG>(p, j, nb_, nks_, ntm_, ntn_, nv_); ++j) {
+          if (!nv_) continue;
+          if (--need == 0) {
+            if (ntn_ != tn || nb_ != b) {
+              fetch_st(ntn_, nb_, pf_s, pf_t);
+              pf_tn = ntn_;
+              pf_b = nb_;
+            }
+            break;
           }
-          colbuf[c] = sv;
-          colbuf[BN + c] = tv;
         }
       }
       if constexpr (GENERIC) {
@@ -1065,11 +1140,17 @@ __global__ void __launch_bounds__(kNumThreads, 1)
           }
       };
       if (GENERIC && p.has_mat && p.split_k == 1) prefetch(0, mat);
-      if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&tfull[grp], acc_phase);
-      else ptx::mbar_wait(&tfull[grp], acc_phase);
-      acc_phase ^= 1u;
+      if (colsplit) {
+        if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&tfull[abuf], acc_phase2[abuf]);
+        else ptx::mbar_wait(&tfull[abuf], acc_phase2[abuf]);
+        acc_phase2[abuf] ^= 1u;
+      } else {
+        if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&tfull[grp], acc_phase);
+        else ptx::mbar_wait(&tfull[grp], acc_phase);
+        acc_phase ^= 1u;
+      }
       ptx::tc_fence_after();
-      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lg * 32) << 16) + grp * BN;
+      const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lg * 32) << 16) + abuf * BN;
       if (lead) detail::trace(p, i, TR_EPI_ACC, t0);
       const int ncols = static_cast<int>(min(static_cast<int64_t>(BN), p.N - n0));  // valid columns
       if (p.split_k > 1) {
@@ -1090,7 +1171,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
             __stcg(dst + q, make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
                                         __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3])));
         }
-        release_acc();  // TMEM is free again: the MMA can start the next unit
+        release_acc(abuf);  // TMEM is free again: the MMA can start the next unit
         __threadfence();
         ptx::named_bar_sync(3 + grp, 128);
         if (gt == 0) split_flag[grp] = (atomicAdd(&p.counters[tile_id], 1) == p.split_k - 1) ? 1u : 0u;
@@ -1126,19 +1207,20 @@ __global__ void __launch_bounds__(kNumThreads, 1)
       if constexpr (!GENERIC) {
         // compact variant (host guarantees: canonical epilogue, bf16 TMA-stored
         // output, residual absent or bf16 contiguous 16-byte aligned with N % 32 == 0)
+        // this group's column half of the tile
+        constexpr int kHalf = BN / 2;
+        const int cofs = grp * kHalf;
+        const int hcols = max(0, min(kHalf, ncols - cofs));
         const uint4* res = nullptr;
         if (p.canon_res_op >= 0)
           res = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.ops[p.canon_res_op].ptr) +
-                                               rowpart[0] + n0);
-        const int32_t cb = static_cast<int32_t>(n0);
-        long long* ftr = (p.trace != nullptr && e == 0 && i < static_cast<uint32_t>(kTraceTiles))
-                             ? p.trace + (static_cast<int64_t>(blockIdx.x) * kTraceTiles + i) * kTraceEvents
-                             : nullptr;
+                                               rowpart[0] + n0 + cofs);
+        const int32_t cb = static_cast<int32_t>(n0) + cofs;
         switch (p.canon_act * 2 + (res != nullptr ? 1 : 0)) {
 #define TMB_DRAIN(A, R)                                                                                          \
   case A * 2 + R:                                                                                                \
-    detail::drain_fast<BN, CG, Cfg::OUT_ROW, A, R>(&tmC, taddr, colbuf, obuf, ncols, cb, row0, b, lane, res,      \
-                                                   &tempty[grp], ftr, t0);                                       \
+    detail::drain_fast<BN, CG, Cfg::OUT_ROW, A, R>(&tmC, taddr + cofs, colbuf + cofs, obuf, hcols, cb, row0, b,  \
+                                                   lane, res, &tempty[abuf]);                                    \
     break;
           TMB_DRAIN(0, 0) TMB_DRAIN(0, 1) TMB_DRAIN(1, 0) TMB_DRAIN(1, 1) TMB_DRAIN(2, 0) TMB_DRAIN(2, 1)
 #undef TMB_DRAIN
@@ -1152,7 +1234,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
         uint32_t r[32];
         ptx::tmem_ld32(taddr + c2 * 32, r);
         ptx::tmem_wait_ld();
-        if ((c2 + 1) * 32 >= ncols) release_acc();
+        if ((c2 + 1) * 32 >= ncols) release_acc(abuf);
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
           const int c = c2 * 32 + hh * 16;
@@ -1262,7 +1344,7 @@ __global__ void __launch_bounds__(kNumThreads, 1)
   if (p.trace != nullptr && threadIdx.x == 0)  // ns: all roles done (tile 0's slot 15)
     p.trace[static_cast<int64_t>(blockIdx.x) * kTraceTiles * kTraceEvents + 15] =
         static_cast<long long>(ptx::globaltimer());
-  if (warp == 4 + kEpiWarps) {
+  if (warp == R::kMmaWarp) {
     if (p.trace != nullptr && lane == 0)  // ns: MMA warp past the barrier (tile 1's slot 14)
       p.trace[(static_cast<int64_t>(blockIdx.x) * kTraceTiles + 1) * kTraceEvents + 14] =
           static_cast<long long>(ptx::globaltimer());

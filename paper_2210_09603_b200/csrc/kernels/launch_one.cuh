@@ -26,24 +26,29 @@ void launch_one(const BoundKernel& k, cudaStream_t s) {
   std::memcpy(&ta, k.tma_a, sizeof(ta));
   std::memcpy(&tb, k.tma_b, sizeof(tb));
   std::memcpy(&tc, k.tma_c, sizeof(tc));
-  if constexpr (CG == 1) {
-    fn<<<k.grid, kNumThreads, Cfg::SMEM_BYTES, s>>>(k.p, ta, tb, tc);
-  } else {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(k.grid);
-    cfg.blockDim = dim3(kNumThreads);
-    cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, fn, k.p, ta, tb, tc) != cudaSuccess)
-      taskmap::fail("cudaLaunchKernelEx (cluster) failed: ", cudaGetErrorString(cudaGetLastError()));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(k.grid);
+  cfg.blockDim = dim3(Roles<GENERIC>::kThreads);
+  cfg.dynamicSmemBytes = Cfg::SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  // programmatic dependent launch: this grid's prologue overlaps the previous
+  // kernel's tail (the kernel waits with griddepcontrol.wait before touching memory)
+  attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[na].val.programmaticStreamSerializationAllowed = 1;
+  ++na;
+  if constexpr (CG == 2) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = CG;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
   }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  if (cudaLaunchKernelEx(&cfg, fn, k.p, ta, tb, tc) != cudaSuccess)
+    taskmap::fail("cudaLaunchKernelEx failed: ", cudaGetErrorString(cudaGetLastError()));
 }
 
 // per-unit dispatchers (defined in inst_*.cu); return false if no variant matches
