@@ -235,6 +235,17 @@ def run_cpu_sample(tasks, threads):
     return sum(t[3] for t in tasks), time.perf_counter() - t0, kind
 
 
+def traffic_of(group):
+    """DRAM bytes per launch of a kernel group from the committed ncu capture
+    (profiles/traffic.json, scripts/traffic_from_launches.py), else None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)[group]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 # -------------------------------------------------------------------- main --
 def main():
     ap = argparse.ArgumentParser()
@@ -248,6 +259,8 @@ def main():
                     help="auto: reuse tuning_cache.json entries, tune the rest on the device")
     ap.add_argument("--tuning-cache", default=os.path.join(ROOT, "tuning_cache.json"))
     ap.add_argument("--per-item", action="store_true", help="print per-launch times to stderr")
+    ap.add_argument("--launch-list", action="store_true",
+                    help="replay exactly one step and exit (for the ncu launch list / traffic capture)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
@@ -320,6 +333,12 @@ def main():
         if dist is not None:
             gather_to_root(results, 0, gather_bufs)
 
+    if args.launch_list:
+        step()
+        torch.cuda.synchronize()
+        print(json.dumps({"launch_list": True, "launches_per_step": sum(it["exec"].num_launches for it in items),
+                          "names": [it["name"] for it in items]}))
+        return
     for _ in range(args.warmup):
         step()
         gather()
@@ -449,7 +468,8 @@ def main():
                               "space_size": len(schedule_space("matmul"))}},
         "roofline": {"bound": "tensor", "kernel": f"tm_gemm_kernel ({dom} launches)",
                      "achieved": dg["tflops"], "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": dg["tflops"] / peak_tf, "traffic": None,
+                     "frac": dg["tflops"] / peak_tf, "traffic": traffic_of(dom),
+                     "algorithmic_bytes_per_launch": dg["bytes"] / max(1, dg["launches"]),
                      "peak_source": f"{peak_src} bf16 burst"},
         "breakdown": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                       for k, v in groups.items()},

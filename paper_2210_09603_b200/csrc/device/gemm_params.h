@@ -151,6 +151,14 @@ struct GemmParams {
   // [cta][kTraceTiles][kTraceEvents]; null = tracing off
   long long* trace;
   int32_t dbg;  // diagnostics (TMB_DBG): 1 = skip all roles after setup
+  // canonical epilogue with a bf16 TMA-stored output (and bf16 contiguous
+  // residual): drained by the lean drain_fast path in either kernel
+  int32_t epi_fast;
+  // weight-stationary B: one column tile, one batch, no split-K and a ring
+  // depth that is a multiple of num_kb, so k-block kb always lands in the same
+  // ring slot: B is loaded in the first ring pass only and stays resident
+  int32_t b_resident;
+  int32_t ring;  // ring slots in use (0 = all STAGES)
   int32_t n_ops;
   int32_t has_mat;  // any SIDE_MAT op
   int32_t out_dtype;

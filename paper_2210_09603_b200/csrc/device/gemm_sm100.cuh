@@ -30,6 +30,10 @@ constexpr int kBM = 128;          // tile rows (TMEM lanes)
 constexpr int kRowBytes = 128;    // one swizzle-128B row of K
 constexpr int kEpiWarps = 8;       // epilogue warps (2 groups x 4 TMEM lane groups)
 constexpr int kNumThreads = 32 * (4 + kEpiWarps + 1);  // loaders + epilogue + MMA
+// The CTA's task list (tile coordinates), decoded once into shared memory at
+// kernel start instead of by every role for every tile: 8 bytes per task.
+constexpr int kTileListMax = 128;
+constexpr int kTileListBytes = kTileListMax * 8;
 
 // Warp roles.  Generic kernel (13 warps): 0-3 loaders (128 gather threads),
 // 4-11 epilogue, 12 MMA.  Compact kernel (all-TMA operands, 12 warps = 384
@@ -63,7 +67,7 @@ struct GemmCfg {
   static constexpr int OUTBUF_BYTES = kEpiWarps * 32 * OUT_ROW;  // one staging buffer per epilogue warp
   // layout: [STAGES x (A | B)] [outbuf] [barriers 256 B] [colbuf]; the base is
   // 1024-byte aligned (checked at run time) as SWIZZLE_128B requires
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + OUTBUF_BYTES + 256 + COLBUF_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + OUTBUF_BYTES + 256 + COLBUF_BYTES + kTileListBytes;
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 must be 16..256 step 16");
 };
 
@@ -72,7 +76,8 @@ constexpr int kMaxSmem = 232448;  // 227 KB opt-in dynamic shared memory per CTA
 // deepest ring (<= 8 stages) that fits next to the epilogue buffers
 constexpr int stages_for(int bn, int cg, bool generic = true) {
   const int stage = kBM * kRowBytes + (bn / cg) * kRowBytes;
-  const int fixed = kEpiWarps * 32 * out_stage_row_bytes(bn, cg) + 256 + 2 * (generic ? kMaxEpiOps : 2) * bn * 4;
+  const int fixed = kEpiWarps * 32 * out_stage_row_bytes(bn, cg) + 256 + 2 * (generic ? kMaxEpiOps : 2) * bn * 4 +
+                    kTileListBytes;
   const int n = (kMaxSmem - fixed) / stage;
   return n > 8 ? 8 : n;
 }
@@ -643,8 +648,8 @@ __device__ __forceinline__ void trace(const GemmParams& p, uint32_t i, int ev, l
 }
 
 template <int CG>
-__device__ __forceinline__ bool next_tile(const GemmParams& p, uint32_t i, int& b, int& ks, int& tm_,
-                                          int& tn, bool& valid) {
+__device__ __forceinline__ bool decode_tile(const GemmParams& p, uint32_t i, int& b, int& ks, int& tm_, int& tn,
+                                            bool& valid) {
   if (i >= p.tile_map.tasks) return false;
   int32_t c[tm::kMaxRank];
   tm::dev_task_fixed<2, 3>(p.tile_map, blockIdx.x / CG, i, c);  // workers = CTA pairs when CG == 2
@@ -653,6 +658,27 @@ __device__ __forceinline__ bool next_tile(const GemmParams& p, uint32_t i, int& 
   tm_ = c[1];
   tn = c[2];
   valid = b < p.batch && tm_ < p.tiles_m && tn < p.tiles_n;
+  return true;
+}
+
+__device__ __forceinline__ bool use_tile_list(const GemmParams& p) {
+  return p.tile_map.tasks <= static_cast<uint32_t>(kTileListMax) && p.tiles_m < 65536 && p.tiles_n < 65536;
+}
+
+// task i of this CTA from the shared-memory list (entry: tm:16 | tn:16 | b*split_k+ks:31 | valid:1),
+// or decoded when the list overflowed
+template <int CG>
+__device__ __forceinline__ bool next_tile(const GemmParams& p, const uint2* list, uint32_t i, int& b, int& ks,
+                                          int& tm_, int& tn, bool& valid) {
+  if (i >= p.tile_map.tasks) return false;
+  if (!use_tile_list(p)) return decode_tile<CG>(p, i, b, ks, tm_, tn, valid);
+  const uint2 e = list[i];
+  tm_ = static_cast<int>(e.x & 0xFFFFu);
+  tn = static_cast<int>(e.x >> 16);
+  const int bk = static_cast<int>(e.y >> 1);
+  b = bk / p.split_k;
+  ks = bk - b * p.split_k;
+  valid = (e.y & 1u) != 0u;
   return true;
 }
 
@@ -679,6 +705,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint32_t* split_flag = tmem_slot + 1;  // [2], one per epilogue warp group
   float* colbuf_all = reinterpret_cast<float*>(outbuf + Cfg::OUTBUF_BYTES + 256);
+  uint2* tile_list = reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(colbuf_all) + Cfg::COLBUF_BYTES);
 
   const uint64_t gt_entry = p.trace != nullptr ? ptx::globaltimer() : 0;
   const int warp = threadIdx.x >> 5;
@@ -691,17 +718,28 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
     if (a_tma) ptx::tma_prefetch_desc(&tmA);
     if (b_tma) ptx::tma_prefetch_desc(&tmB);
     for (int s = 0; s < STAGES; ++s) {
-      ptx::mbar_init(&full[s], all_tma ? 2 : 128);  // all-TMA: the A and B issuing warps
+      // all-TMA: the A and B issuing warps; gather: every loader thread (dbg 4: one per warp)
+      ptx::mbar_init(&full[s], all_tma ? 2 : (p.dbg == 4 ? 4 : 128));
       ptx::mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
       // drained by: the group's 4 warps, or all 8 when the groups split columns (of both CTAs)
-      ptx::mbar_init(&tempty[a], (!GENERIC && p.split_k == 1 ? 8 : 4) * CG);
+      ptx::mbar_init(&tempty[a], ((!GENERIC || p.epi_fast) && p.split_k == 1 ? 8 : 4) * CG);
     }
     ptx::fence_mbar_init();
   }
   using R = Roles<GENERIC>;
+  if (detail::use_tile_list(p)) {
+    for (uint32_t i = threadIdx.x; i < p.tile_map.tasks; i += blockDim.x) {
+      int b, ks, tm_, tn;
+      bool valid;
+      detail::decode_tile<CG>(p, i, b, ks, tm_, tn, valid);
+      tile_list[i] = valid ? make_uint2(static_cast<uint32_t>(tm_) | (static_cast<uint32_t>(tn) << 16),
+                                        (static_cast<uint32_t>(b * p.split_k + ks) << 1) | 1u)
+                           : make_uint2(0u, 0u);
+    }
+  }
   if (warp == R::kMmaWarp) {
     if constexpr (CG == 2) ptx::tmem_alloc_2sm<Cfg::TMEM_COLS>(tmem_slot);
     else ptx::tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
@@ -717,6 +755,8 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
   // for the previous grid, and let the next one start placing CTAs.
   ptx::griddep_launch_dependents();
   ptx::griddep_wait();
+  // ring depth in use (a multiple of num_kb for weight-stationary B, else STAGES)
+  const int ring = (p.ring > 0 && p.ring <= STAGES) ? p.ring : STAGES;
   const long long t0 = clock64();
   if (p.trace != nullptr && threadIdx.x == 0) {  // ns: kernel entry, setup done (tile 0's slots 7, 14)
     long long* tr0 = p.trace + static_cast<int64_t>(blockIdx.x) * kTraceTiles * kTraceEvents;
@@ -743,7 +783,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
       uint32_t q = 0;  // ring slot sequence number
       int b, ks, tm_, tn;
       bool valid;
-      for (uint32_t i = 0; detail::next_tile<CG>(p, i, b, ks, tm_, tn, valid); ++i) {
+      for (uint32_t i = 0; detail::next_tile<CG>(p, tile_list, i, b, ks, tm_, tn, valid); ++i) {
         if (!valid) continue;
         // this CTA's rows of A and columns of B (half of each tile's B when CG == 2)
         const int m0 = tm_ * kTileM + rank * kBM, n0 = tn * BN + rank * (BN / CG);
@@ -757,6 +797,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
           uint8_t* a_tile = smA + stage * Cfg::A_BYTES;
           uint8_t* b_tile = smB + stage * Cfg::B_BYTES;
           const int k0 = kb * BK;
+          const bool b_stays = p.b_resident && q >= static_cast<uint32_t>(ring);
           if (all_tma) {
             // slot q: A from warp 2q mod 4, B from warp 2q+1 mod 4 (full barrier count 2)
             const bool do_a = (2u * q) % R::kLoadWarps == lw, do_b = (2u * q + 1u) % R::kLoadWarps == lw;
@@ -790,7 +831,9 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
                                                 static_cast<uint16_t>(fh));
                   }
                 }
-                if (do_b) {
+                if (do_b && b_stays) {
+                  if (rank == 0) ptx::mbar_arrive(&full[stage]);  // B already resident in this slot
+                } else if (do_b) {
                   if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], CG * Cfg::B_BYTES);
                   if (p.b_loader == LD_TMA_K) {
                     ptx::tma_load_3d_2sm(b_tile, &tmB, lead_full, k0, n0, b);
@@ -834,7 +877,9 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
                     }
                   }
                 }
-                if (do_b) {
+                if (do_b && b_stays) {
+                  ptx::mbar_arrive(&full[stage]);  // B already resident in this slot
+                } else if (do_b) {
                   ptx::mbar_arrive_expect_tx(&full[stage], Cfg::B_BYTES);
                   if (p.b_loader == LD_TMA_K) {
                     ptx::tma_load_3d(b_tile, &tmB, &full[stage], k0, n0, b);
@@ -846,7 +891,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
                 }
               }
             }
-            if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+            if (++stage == ring) { stage = 0; phase ^= 1u; }
             continue;
           }
           // ---- mixed / gather mode (GENERIC): lane 0 of warp q % 4 issues the slot's
@@ -859,7 +904,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
           }
           if (issuer) {
             // mixed mode: announce the TMA bytes now, arrive after the gather
-            const uint32_t tx = (a_tma ? Cfg::A_BYTES : 0) + (b_tma ? Cfg::B_BYTES : 0);
+            const uint32_t tx = (a_tma ? Cfg::A_BYTES : 0) + (b_tma && !b_stays ? Cfg::B_BYTES : 0);
             if (tx) ptx::mbar_expect_tx(&full[stage], tx);
           }
           if (issuer) {
@@ -893,7 +938,9 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
                                         static_cast<uint16_t>(tap % p.conv.kw), static_cast<uint16_t>(tap / p.conv.kw));
               }
             }
-            if (p.b_loader == LD_TMA_K) {
+            if (b_stays) {
+              // weight-stationary: this slot's B is already resident
+            } else if (p.b_loader == LD_TMA_K) {
               ptx::tma_load_3d(b_tile, &tmB, &full[stage], k0, n0, b);
             } else if (p.b_loader == LD_TMA_MN) {
 #pragma unroll 1
@@ -911,13 +958,13 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
                 detail::gather_row_strided<TF32, BK>(a_tile, t, p.a, row, ok, b, k0, p.K);
               else if (p.a_loader == LD_IM2COL_G8) {
                 if constexpr (!TF32) {
-                  if (p.dbg != 3) detail::gather_g8<BK>(a_tile, t, p.conv, g8, kb);  // async, arrives below
+                  if (p.dbg != 3 && p.dbg != 4) detail::gather_g8<BK>(a_tile, t, p.conv, g8, kb);  // async, arrives below
                 }
               } else {
                 detail::gather_row_im2col<TF32, BK>(a_tile, t, p.conv, row, ok, k0, p.K);
               }
             }
-            if (!b_tma) {
+            if (!b_tma && !b_stays) {
 #pragma unroll 1
               for (int r = t; r < BN; r += 128) {
                 const int64_t row = n0 + r;
@@ -928,7 +975,10 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
                   detail::gather_row_filter<TF32, BK>(b_tile, r, p.conv, row, ok, k0, p.K);
               }
             }
-            if (p.a_loader == LD_IM2COL_G8 && b_tma) {
+            if (p.dbg == 4) {  // diagnostics: no gather, one arrival per warp
+              __syncwarp();
+              if ((t & 31) == 0) ptx::mbar_arrive(&full[stage]);
+            } else if (p.a_loader == LD_IM2COL_G8 && b_tma) {
               ptx::cp_async_arrive_noinc(&full[stage]);  // when this thread's copies land
             } else {
               if (p.a_loader == LD_IM2COL_G8) asm volatile("cp.async.wait_all;" ::: "memory");
@@ -936,7 +986,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
               ptx::mbar_arrive(&full[stage]);
             }
           }
-          if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+          if (++stage == ring) { stage = 0; phase ^= 1u; }
         }
       }
     }
@@ -1021,7 +1071,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
       }
     };
     uint32_t nvalid = 0;
-    const bool colsplit = !GENERIC && p.split_k == 1;
+    const bool colsplit = (!GENERIC || p.epi_fast) && p.split_k == 1;
     uint32_t acc_phase2[2] = {0u, 0u};  // colsplit: per-buffer phase
     // canonical S / T of columns gt and gt + 128 of tile column block tn_ (batch b_)
     auto fetch_st = [&](int tn_, int b_, float (&s_v)[2], float (&t_v)[2]) {
@@ -1043,7 +1093,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
     };
     float pf_s[2] = {0.f, 0.f}, pf_t[2] = {0.f, 0.f};
     int pf_tn = -1, pf_b = -1;
-    for (uint32_t i = 0; detail::next_tile<CG>(p, i, b, ks, tm_, tn, valid); ++i) {
+    for (uint32_t i = 0; detail::next_tile<CG>(p, tile_list, i, b, ks, tm_, tn, valid); ++i) {
       if (!valid) continue;
       // accumulator buffer = tile parity.  Compact kernel (no split-K): both groups
       // drain every tile, group g the column half g (a tile's drain takes half as
@@ -1085,7 +1135,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
         int nb_, nks_, ntm_, ntn_;
         bool nv_;
         uint32_t need = colsplit ? 1u : 2u;
-        for (uint32_t j = i + 1; detail::next_tile<CG>(p, j, nb_, nks_, ntm_, ntn_, nv_); ++j) {
+        for (uint32_t j = i + 1; detail::next_tile<CG>(p, tile_list, j, nb_, nks_, ntm_, ntn_, nv_); ++j) {
           if (!nv_) continue;
           if (--need == 0) {
             if (ntn_ != tn || nb_ != b) {
@@ -1139,7 +1189,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
             }
           }
       };
-      if (GENERIC && p.has_mat && p.split_k == 1) prefetch(0, mat);
+      if (GENERIC && !colsplit && p.has_mat && p.split_k == 1) prefetch(0, mat);
       if (colsplit) {
         if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&tfull[abuf], acc_phase2[abuf]);
         else ptx::mbar_wait(&tfull[abuf], acc_phase2[abuf]);
@@ -1204,8 +1254,8 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
       }
       // 32 columns per TMEM load; the accumulator is released right after the
       // last load, before the math of the last columns
-      if constexpr (!GENERIC) {
-        // compact variant (host guarantees: canonical epilogue, bf16 TMA-stored
+      if (colsplit) {
+        // lean drain (host guarantees via epi_fast: canonical epilogue, bf16 TMA-stored
         // output, residual absent or bf16 contiguous 16-byte aligned with N % 32 == 0)
         // this group's column half of the tile
         constexpr int kHalf = BN / 2;
@@ -1214,7 +1264,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
         const uint4* res = nullptr;
         if (p.canon_res_op >= 0)
           res = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.ops[p.canon_res_op].ptr) +
-                                               rowpart[0] + n0 + cofs);
+                                               detail::addr_rowpart(p.ops[p.canon_res_op].a, rr, b) + n0 + cofs);
         const int32_t cb = static_cast<int32_t>(n0) + cofs;
         switch (p.canon_act * 2 + (res != nullptr ? 1 : 0)) {
 #define TMB_DRAIN(A, R)                                                                                          \
@@ -1289,7 +1339,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
       uint32_t acc_phase = 0;
       int b, ks, tm_, tn;
       bool valid;
-      for (uint32_t i = 0; detail::next_tile<CG>(p, i, b, ks, tm_, tn, valid); ++i) {
+      for (uint32_t i = 0; detail::next_tile<CG>(p, tile_list, i, b, ks, tm_, tn, valid); ++i) {
         if (!valid) continue;
         if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&tempty[acc], acc_phase ^ 1u);
         else ptx::mbar_wait(&tempty[acc], acc_phase ^ 1u);
@@ -1298,7 +1348,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
         for (int kb0 = ks * p.kb_per_split, kb = kb0, kb_end = min(p.num_kb, kb0 + p.kb_per_split); kb < kb_end; ++kb) {
           if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&full[stage], phase);
           else ptx::mbar_wait(&full[stage], phase);
-          if (GENERIC && !all_tma) ptx::fence_proxy_async_smem();  // cp.async (generic proxy) -> tcgen05.mma
+          if (GENERIC && !all_tma && p.dbg != 5) ptx::fence_proxy_async_smem();  // cp.async (generic proxy) -> tcgen05.mma
           ptx::tc_fence_after();
           if (kb == kb0 && lane == 0) detail::trace(p, i, TR_MMA_FIRST, t0);
           const uint64_t ad = adesc0 + static_cast<uint64_t>((stage * Cfg::A_BYTES) >> 4);
@@ -1322,7 +1372,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
             else ptx::mma_commit(&empty[stage]);
           }
           __syncwarp();
-          if (++stage == STAGES) { stage = 0; phase ^= 1u; }
+          if (++stage == ring) { stage = 0; phase ^= 1u; }
         }
         if (ptx::elect_one()) {
           if constexpr (CG == 2) ptx::mma_commit_2sm(&tfull[acc], 0x3);

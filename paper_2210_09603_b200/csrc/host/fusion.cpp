@@ -1019,10 +1019,11 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
                  reinterpret_cast<uintptr_t>(r.ptr) % 16 == 0 && (a.s_hi * 2) % 16 == 0 &&
                  (a.s_lo * 2) % 16 == 0 && (a.s_batch * 2) % 16 == 0 && (a.offset * 2) % 16 == 0;
       }
-      k.generic = (a_t && b_t && p.canon && !k.tf32 && p.out_tma && p.out_dtype == DT_BF16 && res_ok &&
-                   !std::getenv("TMB_GENERIC"))
-                      ? 0
-                      : 1;
+      p.epi_fast = (p.canon && !k.tf32 && p.out_tma && p.out_dtype == DT_BF16 && res_ok &&
+                    !std::getenv("TMB_GENERIC"))
+                       ? 1
+                       : 0;
+      k.generic = (a_t && b_t && p.epi_fast) ? 0 : 1;
     }
     if (const char* sw = std::getenv("TMB_MN_SWAP")) p.mn_lbo_sbo_swap = std::atoi(sw);
     p.fast_math = p.out_dtype != TM_F32;  // approximate tanh only where the output rounding dominates
@@ -1048,6 +1049,14 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
     int used = grid / k.cg;
     p.tile_map = tile_mapping(int64_t(sp.batch) * p.split_k, p.tiles_m, p.tiles_n, grid / k.cg, plan.cfg.raster, used);
     k.grid = used * k.cg;  // workers of the tile mapping are CTA pairs when cg == 2
+    {
+      const int st = kernel_stages(k);
+      p.b_resident = (!k.simt && p.tiles_n == 1 && sp.batch == 1 && p.split_k == 1 && p.num_kb <= st &&
+                      !std::getenv("TMB_NO_BRES"))
+                         ? 1
+                         : 0;
+      p.ring = p.b_resident ? (st / p.num_kb) * p.num_kb : 0;
+    }
     if (const char* d = std::getenv("TMB_DBG")) p.dbg = std::atoi(d);
     if (std::getenv("TMB_TRACE")) {  // per-tile role timeline (tm_exec_trace)
       void* tr = nullptr;

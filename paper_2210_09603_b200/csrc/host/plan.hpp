@@ -94,6 +94,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
 // kernel launcher (gemm_launch.cu)
 int num_sms(int device);
 void launch_bound(const BoundKernel& k, void* stream);
+int kernel_stages(const BoundKernel& k);  // ring depth of the instantiation launch_bound will pick
 void pack_filter(const ConvGeom& g, int kp, void* out);  // bf16 [f][kp] in the GEMM K order
 void launch_simt(const BoundKernel& k, void* stream);   // fp32 CUDA-core kernel (simt_fp32.cu)
 int kernel_mapping_assign(int which, uint32_t worker, int* buf, int cap);

@@ -185,6 +185,14 @@ float device_max_rel_error(const void* a, const void* b, size_t n, int dtype, vo
   return f;
 }
 
+int kernel_stages(const BoundKernel& k) {
+  if (k.simt) return 2;
+  if (k.cg == 2) return k.tf32 || k.generic ? stages_for(k.bn, 2) : stages_for(k.bn, 2, false);
+  const bool deep = k.stages == 0 || k.stages > 2;
+  if (!deep) return 2;
+  return k.tf32 ? stages_for(k.bn, 1) : stages_for(k.bn, 1, k.generic != 0);
+}
+
 void launch_bound(const BoundKernel& k, void* stream) {
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   bool ok;
