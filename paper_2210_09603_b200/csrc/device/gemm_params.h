@@ -159,6 +159,9 @@ struct GemmParams {
   // ring slot: B is loaded in the first ring pass only and stays resident
   int32_t b_resident;
   int32_t ring;  // ring slots in use (0 = all STAGES)
+  // lean drain writes bf16 rows straight from registers (16-byte stores) instead
+  // of smem staging + TMA store: row-major output, 16-byte aligned rows, N % 8 == 0
+  int32_t out_direct;
   int32_t n_ops;
   int32_t has_mat;  // any SIDE_MAT op
   int32_t out_dtype;

@@ -551,11 +551,24 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return d;
 }
 
+#ifdef TMB_FINE_TRACE
+// diagnostics build only (-DTMB_FINE_TRACE): clock64 at each drain step of the
+// first epilogue warp, into trace rows 48.. of the CTA (tracing must be on)
+#define TMB_FT(i) do { if (fine != nullptr && threadIdx.x == 128 && (i) < 256) fine[(i)] = clock64(); } while (0)
+#else
+#define TMB_FT(i) do { } while (0)
+#endif
+
 template <int BN, int CG, int OUT_ROW, int ACT, bool RES>
 __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t taddr, const float* colbuf,
                                            uint8_t* obuf, int ncols, int32_t col_base, int32_t row0,
-                                           int32_t b, int lane, const uint4* res, uint64_t* tempty_bar) {
+                                           int32_t b, int lane, const uint4* res, uint64_t* tempty_bar,
+                                           long long* fine = nullptr, __nv_bfloat16* drow = nullptr,
+                                           int dcols = 0) {
   constexpr int GC = OUT_ROW / 2;  // bf16 columns per TMA store group (32 or 64)
+  int ft = 0;
+  (void)fine;
+  (void)ft;
   auto release = [&]() {  // the MMA may reuse this accumulator buffer
     ptx::tc_fence_before();
     __syncwarp();
@@ -579,6 +592,7 @@ __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t tadd
 #pragma unroll 1
   for (int c = 0; c < ncols; c += 32) {
     uint32_t r[32];
+    TMB_FT(ft++);
     ptx::tmem_ld32(taddr + c, r);
     uint4 rn[4];
     if constexpr (RES) {
@@ -588,11 +602,13 @@ __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t tadd
       }
     }
     ptx::tmem_wait_ld();
+    TMB_FT(ft++);
     if (c + 32 >= ncols) release();  // last TMEM read of this tile
-    if (c % GC == 0) {  // the previous store from this buffer has read it
+    if (drow == nullptr && dcols >= 0 && c % GC == 0) {  // the previous store from this buffer has read it
       if (lane == 0) ptx::bulk_wait_read<0>();
       __syncwarp();
     }
+    TMB_FT(ft++);
     uint32_t w[16];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -621,10 +637,27 @@ __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t tadd
       w[2 * q] = pack_bf16x2(x[0], x[1]);
       w[2 * q + 1] = pack_bf16x2(x[2], x[3]);
     }
+    TMB_FT(ft++);
+    if (drow != nullptr || dcols < 0) {
+      // direct: this lane's row segment straight from registers (16-byte stores,
+      // whole 32-byte sectors over the 4 stores); no staging, proxy fence or TMA
+      if (drow != nullptr) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (c + 8 * k < dcols)
+            *reinterpret_cast<uint4*>(drow + c + 8 * k) = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+      }
+      if constexpr (RES) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rq[q] = rn[q];
+      }
+      continue;
+    }
     const int j0 = (c % GC) / 8;  // first 16-byte chunk of these 32 columns in the staged row
 #pragma unroll
     for (int k = 0; k < 4; ++k)
       *reinterpret_cast<uint4*>(orow + (((j0 + k) ^ swz) << 4)) = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+    TMB_FT(ft++);
     if ((c + 32) % GC == 0 || c + 32 >= ncols) {
       ptx::fence_proxy_async_smem();
       __syncwarp();
@@ -633,6 +666,7 @@ __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t tadd
         ptx::bulk_commit();
       }
     }
+    TMB_FT(ft++);
     if constexpr (RES) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) rq[q] = rn[q];
@@ -1266,11 +1300,28 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
           res = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.ops[p.canon_res_op].ptr) +
                                                detail::addr_rowpart(p.ops[p.canon_res_op].a, rr, b) + n0 + cofs);
         const int32_t cb = static_cast<int32_t>(n0) + cofs;
+        // direct stores (p.out_direct): this lane's row of the output; dcols = valid
+        // columns of the half (multiple of 8 by the host's check), -1 = row outside M
+        __nv_bfloat16* drow = nullptr;
+        int dcols = 0;
+        if (p.out_direct) {
+          if (row_ok) {
+            drow = static_cast<__nv_bfloat16*>(p.out) + detail::addr_rowpart(p.out_a, rr, b) + n0 + cofs;
+            dcols = hcols;
+          } else {
+            dcols = -1;
+          }
+        }
+        long long* fine = nullptr;
+#ifdef TMB_FINE_TRACE
+        if (p.trace != nullptr && nvalid <= 4)
+          fine = p.trace + (static_cast<int64_t>(blockIdx.x) * kTraceTiles + 48) * kTraceEvents + (nvalid - 1) * 64;
+#endif
         switch (p.canon_act * 2 + (res != nullptr ? 1 : 0)) {
 #define TMB_DRAIN(A, R)                                                                                          \
   case A * 2 + R:                                                                                                \
     detail::drain_fast<BN, CG, Cfg::OUT_ROW, A, R>(&tmC, taddr + cofs, colbuf + cofs, obuf, hcols, cb, row0, b,  \
-                                                   lane, res, &tempty[abuf]);                                    \
+                                                   lane, res, &tempty[abuf], fine, drow, dcols);                 \
     break;
           TMB_DRAIN(0, 0) TMB_DRAIN(0, 1) TMB_DRAIN(1, 0) TMB_DRAIN(1, 1) TMB_DRAIN(2, 0) TMB_DRAIN(2, 1)
 #undef TMB_DRAIN

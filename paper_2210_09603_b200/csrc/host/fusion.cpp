@@ -1024,6 +1024,16 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
                        ? 1
                        : 0;
       k.generic = (a_t && b_t && p.epi_fast) ? 0 : 1;
+      // direct register -> global stores for the lean drain: opt-in (TMB_OUT_DIRECT=1); measured
+      // slower than smem staging + TMA store on every sweep shape
+      {
+        const Addr& a = p.out_a;
+        p.out_direct = (p.epi_fast && a.s_col == 1 && p.N % 8 == 0 && reinterpret_cast<uintptr_t>(p.out) % 16 == 0 &&
+                        (a.s_hi * 2) % 16 == 0 && (a.s_lo * 2) % 16 == 0 && (a.s_batch * 2) % 16 == 0 &&
+                        (a.offset * 2) % 16 == 0 && std::getenv("TMB_OUT_DIRECT"))
+                           ? 1
+                           : 0;
+      }
     }
     if (const char* sw = std::getenv("TMB_MN_SWAP")) p.mn_lbo_sbo_swap = std::atoi(sw);
     p.fast_math = p.out_dtype != TM_F32;  // approximate tanh only where the output rounding dominates
