@@ -106,6 +106,45 @@ def test_matmul_bf16_output():
     assert port.max_rel_error(got["D"], port.matmul_bias_relu(a, b, rounded(bias, "bf16"))) <= 1e-2
 
 
+@pytest.mark.parametrize("bm,bn", [(128, 64), (128, 128), (128, 192), (128, 256), (256, 128), (256, 256)])
+@pytest.mark.parametrize("mn", [(333, 200), (640, 520)])
+def test_lean_drain_bf16_output_exact(bm, bn, mn):
+    """bf16 TMA-stored output + canonical epilogue: the lean drain path, the two
+    epilogue warp groups each draining one column half of every tile (ragged M/N:
+    half tiles that are partly or wholly outside N).  Integer data keeps every
+    fp32 intermediate exact, so the device must equal round_bf16(reference)."""
+    m, n = mn
+    k = 320
+    a, b, bias = _matmul_case(m, n, k, True, 41)
+    dag = matmul_epilogue_dag(m, n, k, DType.I32)
+    got, _ = run(dag, {"A": dev(a), "B": dev(b), "Bias": dev(bias, "f32")}, {"D": (m, n)}, out_dtype="bf16",
+                 cfg=ScheduleConfig(block_m=bm, block_n=bn))
+    assert np.array_equal(got["D"], port.round_bf16(port.matmul_bias_relu(a, b, bias)))
+
+
+@pytest.mark.parametrize("bn", [128, 256])
+def test_lean_drain_residual_exact(bn):
+    """D = relu(A B + bias) + R with a bf16 residual (the FFN's second GEMM form)."""
+    import torch
+    from paper_2210_09603_b200 import Axis, Plan, add, load, relu, var
+    from paper_2210_09603_b200 import matmul_dag
+    m, n, k = 384, 320, 256
+    a, b, bias = _matmul_case(m, n, k, True, 43)
+    r = port.Rng(44).tensor((m, n), True)
+    dag = matmul_dag(m, n, k, DType.I32)
+    dag.add_input("Bias", [n], DType.I32)
+    dag.add_input("R", [m, n], DType.I32)
+    dag.add_compute("D", [Axis("i", m), Axis("j", n)],
+                    add(relu(add(load("C", [var("i"), var("j")]), load("Bias", [var("j")]))),
+                        load("R", [var("i"), var("j")])), DType.I32)
+    dag.outputs = ["D"]
+    out = torch.full((m, n), float("nan"), dtype=torch.bfloat16, device="cuda")
+    Plan(dag, ScheduleConfig(block_n=bn)).bind([dev(a), dev(b), dev(bias, "f32"), dev(r)], [out]).launch()
+    torch.cuda.synchronize()
+    want = port.round_bf16(port.matmul_bias_relu(a, b, bias) + r)
+    assert np.array_equal(out.float().cpu().numpy().astype(np.float64), want)
+
+
 @pytest.mark.parametrize("mnk", [(2039, 2039, 2039), (1, 1, 1), (130, 17, 5), (7, 300, 77)])
 def test_matmul_prime_and_tiny_sizes(mnk):
     """any M,N,K >= 1 (2039^3 is where input-centric spaces fail)."""
