@@ -151,6 +151,10 @@ struct GemmParams {
   // [cta][kTraceTiles][kTraceEvents]; null = tracing off
   long long* trace;
   int32_t dbg;  // diagnostics (TMB_DBG): 1 = skip all roles after setup
+  int32_t dbg_skip;
+  // per-worker task list precomputed at bind time ([workers][tile_map.tasks] of
+  // {tm | tn << 16, (b * split_k + ks) << 1 | valid}); null = decode on device
+  const uint32_t* tile_tab;  // diagnostics with dbg 1 (TMB_SKIP bits): 1 tile list, 2 barrier init, 4 TMEM
   // canonical epilogue with a bf16 TMA-stored output (and bf16 contiguous
   // residual): drained by the lean drain_fast path in either kernel
   int32_t epi_fast;

@@ -748,7 +748,8 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
   const bool b_tma = p.b_loader == LD_TMA_K || p.b_loader == LD_TMA_MN;
   const bool all_tma = a_tma && b_tma;
 
-  if (threadIdx.x == 0) {
+  const int skip = p.dbg == 1 ? p.dbg_skip : 0;
+  if (threadIdx.x == 0 && !(skip & 2)) {
     if (a_tma) ptx::tma_prefetch_desc(&tmA);
     if (b_tma) ptx::tma_prefetch_desc(&tmB);
     for (int s = 0; s < STAGES; ++s) {
@@ -764,7 +765,11 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
     ptx::fence_mbar_init();
   }
   using R = Roles<GENERIC>;
-  if (detail::use_tile_list(p)) {
+  if (detail::use_tile_list(p) && p.tile_tab != nullptr) {
+    // the bind-time table: one 8-byte load per task (L2-resident after the first launch)
+    const uint2* tab = reinterpret_cast<const uint2*>(p.tile_tab) + static_cast<size_t>(blockIdx.x / CG) * p.tile_map.tasks;
+    for (uint32_t i = threadIdx.x; i < p.tile_map.tasks; i += blockDim.x) tile_list[i] = __ldg(tab + i);
+  } else if (detail::use_tile_list(p) && !(skip & 1)) {
     for (uint32_t i = threadIdx.x; i < p.tile_map.tasks; i += blockDim.x) {
       int b, ks, tm_, tn;
       bool valid;
@@ -774,7 +779,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
                            : make_uint2(0u, 0u);
     }
   }
-  if (warp == R::kMmaWarp) {
+  if (warp == R::kMmaWarp && !(skip & 4)) {
     if constexpr (CG == 2) ptx::tmem_alloc_2sm<Cfg::TMEM_COLS>(tmem_slot);
     else ptx::tmem_alloc<Cfg::TMEM_COLS>(tmem_slot);
   }
@@ -1450,8 +1455,10 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
       p.trace[(static_cast<int64_t>(blockIdx.x) * kTraceTiles + 1) * kTraceEvents + 14] =
           static_cast<long long>(ptx::globaltimer());
     ptx::tc_fence_after();
-    if constexpr (CG == 2) ptx::tmem_dealloc_2sm<Cfg::TMEM_COLS>(tmem_base);
-    else ptx::tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+    if (!(skip & 4)) {
+      if constexpr (CG == 2) ptx::tmem_dealloc_2sm<Cfg::TMEM_COLS>(tmem_base);
+      else ptx::tmem_dealloc<Cfg::TMEM_COLS>(tmem_base);
+    }
     if (p.trace != nullptr && lane == 0)  // ns: TMEM released (tile 1's slot 15)
       p.trace[(static_cast<int64_t>(blockIdx.x) * kTraceTiles + 1) * kTraceEvents + 15] =
           static_cast<long long>(ptx::globaltimer());

@@ -1059,6 +1059,28 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
     int used = grid / k.cg;
     p.tile_map = tile_mapping(int64_t(sp.batch) * p.split_k, p.tiles_m, p.tiles_n, grid / k.cg, plan.cfg.raster, used);
     k.grid = used * k.cg;  // workers of the tile mapping are CTA pairs when cg == 2
+    // per-worker task lists, decoded once here instead of in every CTA of every launch
+    if (p.tile_map.tasks <= 128 && p.tiles_m < 65536 && p.tiles_n < 65536 && !std::getenv("TMB_NO_TILE_TAB")) {
+      const uint32_t workers = p.tile_map.workers, tasks = p.tile_map.tasks;
+      std::vector<uint32_t> tab(size_t(workers) * tasks * 2, 0u);
+      for (uint32_t w = 0; w < workers; ++w)
+        for (uint32_t i = 0; i < tasks; ++i) {
+          int32_t c[tm::kMaxRank];
+          tm::dev_task_fixed<2, 3>(p.tile_map, w, i, c);
+          const int b = c[0] / p.split_k, ks = c[0] % p.split_k;
+          if (b < p.batch && c[1] < p.tiles_m && c[2] < p.tiles_n) {
+            const size_t e = (size_t(w) * tasks + i) * 2;
+            tab[e] = static_cast<uint32_t>(c[1]) | (static_cast<uint32_t>(c[2]) << 16);
+            tab[e + 1] = (static_cast<uint32_t>(b * p.split_k + ks) << 1) | 1u;
+          }
+        }
+      void* d = nullptr;
+      if (cudaMalloc(&d, tab.size() * 4) != cudaSuccess ||
+          cudaMemcpy(d, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+        fail("cudaMalloc/cudaMemcpy failed for the tile table");
+      ex->scratch.push_back(d);
+      p.tile_tab = static_cast<const uint32_t*>(d);
+    }
     {
       const int st = kernel_stages(k);
       p.b_resident = (!k.simt && p.tiles_n == 1 && sp.batch == 1 && p.split_k == 1 && p.num_kb <= st &&
@@ -1068,6 +1090,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       p.ring = p.b_resident ? (st / p.num_kb) * p.num_kb : 0;
     }
     if (const char* d = std::getenv("TMB_DBG")) p.dbg = std::atoi(d);
+    if (const char* d = std::getenv("TMB_SKIP")) p.dbg_skip = std::atoi(d);
     if (std::getenv("TMB_TRACE")) {  // per-tile role timeline (tm_exec_trace)
       void* tr = nullptr;
       const size_t bytes = size_t(k.grid) * kTraceTiles * kTraceEvents * 8;
