@@ -674,6 +674,85 @@ __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t tadd
   }
 }
 
+// Split-K final unit, lean form: sums the split partials of this warp's rows
+// and column half from the fp32 workspace (chunk-major [split][col/16][128][16]),
+// all of a 32-column chunk's loads in flight together, then the same canonical
+// math / bf16 staging / TMA store as drain_fast.
+template <int BN, int CG, int OUT_ROW, int ACT, bool RES>
+__device__ __forceinline__ void drain_reduce(const CUtensorMap* tmC, const float* ws, int split_k, int rloc,
+                                             int cofs, const float* colbuf, uint8_t* obuf, int ncols,
+                                             int32_t col_base, int32_t row0, int32_t b, int lane, const uint4* res) {
+  constexpr int GC = OUT_ROW / 2;
+  uint8_t* const orow = obuf + lane * OUT_ROW;
+  const int swz = OUT_ROW == 128 ? (lane & 7) : ((lane >> 1) & 3);
+#pragma unroll 1
+  for (int c = 0; c < ncols; c += 32) {
+    float x[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = 0.f;
+#pragma unroll 1
+    for (int sp = 0; sp < split_k; ++sp) {  // fixed order: deterministic
+      const float* base = ws + static_cast<int64_t>(sp) * (kBM * BN);
+      float4 f[8];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float4* src = reinterpret_cast<const float4*>(
+            base + (static_cast<int64_t>((cofs + c) / 16 + h) * kBM + rloc) * 16);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) f[4 * h + q] = __ldcg(src + q);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        x[4 * q] += f[q].x; x[4 * q + 1] += f[q].y; x[4 * q + 2] += f[q].z; x[4 * q + 3] += f[q].w;
+      }
+    }
+    uint4 rq[4];
+    if constexpr (RES) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) rq[q] = __ldg(res + c / 8 + q);
+    }
+    if (c % GC == 0) {
+      if (lane == 0) ptx::bulk_wait_read<0>();
+      __syncwarp();
+    }
+    uint32_t w[16];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 sv = *reinterpret_cast<const float4*>(colbuf + c + 4 * q);
+      const float4 tv = *reinterpret_cast<const float4*>(colbuf + BN + c + 4 * q);
+      float y[4] = {fmaf(x[4 * q], sv.x, tv.x), fmaf(x[4 * q + 1], sv.y, tv.y), fmaf(x[4 * q + 2], sv.z, tv.z),
+                    fmaf(x[4 * q + 3], sv.w, tv.w)};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if constexpr (ACT == 1) y[j] = fmaxf(y[j], 0.f);
+        if constexpr (ACT == 2) y[j] = gelu_tanh_fast(y[j]);
+      }
+      if constexpr (RES) {
+        const uint32_t* rw = reinterpret_cast<const uint32_t*>(rq);
+        const uint32_t w0 = rw[2 * q], w1 = rw[2 * q + 1];
+        y[0] += __uint_as_float(w0 << 16);
+        y[1] += __uint_as_float(w0 & 0xFFFF0000u);
+        y[2] += __uint_as_float(w1 << 16);
+        y[3] += __uint_as_float(w1 & 0xFFFF0000u);
+      }
+      w[2 * q] = pack_bf16x2(y[0], y[1]);
+      w[2 * q + 1] = pack_bf16x2(y[2], y[3]);
+    }
+    const int j0 = (c % GC) / 8;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      *reinterpret_cast<uint4*>(orow + (((j0 + k) ^ swz) << 4)) = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+    if ((c + 32) % GC == 0 || c + 32 >= ncols) {
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        ptx::tma_store_3d(tmC, obuf, col_base + (c / GC) * GC, row0, b);
+        ptx::bulk_commit();
+      }
+    }
+  }
+}
+
 // Decodes task `i` of this CTA into (batch, tile_m, tile_n); false once the
 // CTA's task list is exhausted.  Out-of-range tasks are reported via `valid`.
 __device__ __forceinline__ void trace(const GemmParams& p, uint32_t i, int ev, long long t0) {
@@ -760,7 +839,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
       // drained by: the group's 4 warps, or all 8 when the groups split columns (of both CTAs)
-      ptx::mbar_init(&tempty[a], ((!GENERIC || p.epi_fast) && p.split_k == 1 ? 8 : 4) * CG);
+      ptx::mbar_init(&tempty[a], (!GENERIC || p.epi_fast ? 8 : 4) * CG);
     }
     ptx::fence_mbar_init();
   }
@@ -1110,7 +1189,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
       }
     };
     uint32_t nvalid = 0;
-    const bool colsplit = (!GENERIC || p.epi_fast) && p.split_k == 1;
+    const bool colsplit = !GENERIC || p.epi_fast;
     uint32_t acc_phase2[2] = {0u, 0u};  // colsplit: per-buffer phase
     // canonical S / T of columns gt and gt + 128 of tile column block tn_ (batch b_)
     auto fetch_st = [&](int tn_, int b_, float (&s_v)[2], float (&t_v)[2]) {
@@ -1242,6 +1321,55 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lg * 32) << 16) + abuf * BN;
       if (lead) detail::trace(p, i, TR_EPI_ACC, t0);
       const int ncols = static_cast<int>(min(static_cast<int64_t>(BN), p.N - n0));  // valid columns
+      if (p.split_k > 1 && colsplit) {
+        // ---- split-K, lean form: each group parks its column half of the raw partial
+        // tile; the group that completes a (tile, half) last reduces it and stores
+        constexpr int kHalf = BN / 2;
+        const int cofs = grp * kHalf;
+        const int hcols = max(0, min(kHalf, ncols - cofs));
+        const int64_t tile_id = ((static_cast<int64_t>(b) * p.tiles_m + tm_) * p.tiles_n + tn) * CG + rank;
+        const float* ws = p.workspace + tile_id * p.split_k * static_cast<int64_t>(kBM * BN);
+        const int rloc = lg * 32 + lane;
+#pragma unroll 1
+        for (int c = 0; c < kHalf; c += 32) {
+          uint32_t r[32];
+          ptx::tmem_ld32(taddr + cofs + c, r);
+          ptx::tmem_wait_ld();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float4* dst = reinterpret_cast<float4*>(const_cast<float*>(ws) + ks * static_cast<int64_t>(kBM * BN) +
+                                                    (static_cast<int64_t>((cofs + c) / 16 + h) * kBM + rloc) * 16);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              __stcg(dst + q, make_float4(__uint_as_float(r[16 * h + 4 * q]), __uint_as_float(r[16 * h + 4 * q + 1]),
+                                          __uint_as_float(r[16 * h + 4 * q + 2]), __uint_as_float(r[16 * h + 4 * q + 3])));
+          }
+        }
+        release_acc(abuf);  // TMEM is free again: the MMA can start the next unit
+        __threadfence();
+        ptx::named_bar_sync(3 + grp, 128);
+        if (gt == 0) split_flag[grp] = (atomicAdd(&p.counters[tile_id * 2 + grp], 1) == p.split_k - 1) ? 1u : 0u;
+        ptx::named_bar_sync(3 + grp, 128);
+        if (*reinterpret_cast<volatile uint32_t*>(&split_flag[grp]) == 0u) continue;
+        __threadfence();
+        const uint4* res = nullptr;
+        if (p.canon_res_op >= 0)  // rr is row 0 for rows past M (their stores are clipped)
+          res = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.ops[p.canon_res_op].ptr) +
+                                               detail::addr_rowpart(p.ops[p.canon_res_op].a, rr, b) + n0 + cofs);
+        const int32_t cbase = static_cast<int32_t>(n0) + cofs;
+        switch (p.canon_act * 2 + (p.canon_res_op >= 0 ? 1 : 0)) {
+#define TMB_RED(A, R)                                                                                              \
+  case A * 2 + R:                                                                                                  \
+    detail::drain_reduce<BN, CG, Cfg::OUT_ROW, A, R>(&tmC, ws, p.split_k, rloc, cofs, colbuf + cofs, obuf, hcols,  \
+                                                     cbase, row0, b, lane, res);                                   \
+    break;
+          TMB_RED(0, 0) TMB_RED(0, 1) TMB_RED(1, 0) TMB_RED(1, 1) TMB_RED(2, 0) TMB_RED(2, 1)
+#undef TMB_RED
+          default: __trap();
+        }
+        if (gt == 0) p.counters[tile_id * 2 + grp] = 0;  // self-resetting for the next launch
+        continue;
+      }
       if (p.split_k > 1) {
         // ---- split-K: park the raw partial tile, last unit reduces + runs the epilogue
         const int64_t tile_id = ((static_cast<int64_t>(b) * p.tiles_m + tm_) * p.tiles_n + tn) * CG + rank;
@@ -1263,7 +1391,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
         release_acc(abuf);  // TMEM is free again: the MMA can start the next unit
         __threadfence();
         ptx::named_bar_sync(3 + grp, 128);
-        if (gt == 0) split_flag[grp] = (atomicAdd(&p.counters[tile_id], 1) == p.split_k - 1) ? 1u : 0u;
+        if (gt == 0) split_flag[grp] = (atomicAdd(&p.counters[tile_id * 2], 1) == p.split_k - 1) ? 1u : 0u;
         ptx::named_bar_sync(3 + grp, 128);
         if (*reinterpret_cast<volatile uint32_t*>(&split_flag[grp]) == 0u) continue;
         __threadfence();
@@ -1288,7 +1416,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
           if ((c + 1) % (gcols / 16) == 0 || (c + 1) * 16 >= ncols)
             group_end(n0 + (c * 16 / gcols) * gcols, row0);
         }
-        if (gt == 0) p.counters[tile_id] = 0;  // self-resetting for the next launch
+        if (gt == 0) p.counters[tile_id * 2] = 0;  // self-resetting for the next launch
         continue;
       }
       // 32 columns per TMEM load; the accumulator is released right after the

@@ -1047,7 +1047,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
         void* ws = nullptr;
         void* cnt = nullptr;
         if (cudaMalloc(&ws, tiles * p.split_k * 128 * int64_t(k.bn) * 4) != cudaSuccess ||
-            cudaMalloc(&cnt, tiles * 4) != cudaSuccess || cudaMemset(cnt, 0, tiles * 4) != cudaSuccess)
+            cudaMalloc(&cnt, tiles * 8) != cudaSuccess || cudaMemset(cnt, 0, tiles * 8) != cudaSuccess)
           fail("cudaMalloc failed for the split-K workspace");
         ex->scratch.push_back(ws);
         ex->scratch.push_back(cnt);

@@ -122,6 +122,28 @@ def test_lean_drain_bf16_output_exact(bm, bn, mn):
     assert np.array_equal(got["D"], port.round_bf16(port.matmul_bias_relu(a, b, bias)))
 
 
+@pytest.mark.parametrize("bm,bn,split_k", [(128, 128, 2), (128, 256, 3), (256, 128, 2), (128, 64, 4), (128, 192, 3)])
+def test_lean_split_k_bf16_exact(bm, bn, split_k):
+    """Split-K with the lean drain: each epilogue group parks its column half of the
+    partial tile, the last arriver of each (tile, half) reduces in split order and
+    stores bf16; repeated launches reuse the self-resetting counters."""
+    import torch
+    from paper_2210_09603_b200 import Plan
+    m, n, k = 520, 328, 1000
+    a, b, bias = _matmul_case(m, n, k, True, 45)
+    dag = matmul_epilogue_dag(m, n, k, DType.I32)
+    out = torch.empty((m, n), dtype=torch.bfloat16, device="cuda")
+    ex = Plan(dag, ScheduleConfig(block_m=bm, block_n=bn, split_k=split_k)).bind(
+        [dev(a), dev(b), dev(bias, "f32")], [out])
+    assert ex.kernel_info(0)["split_k"] == split_k
+    want = port.round_bf16(port.matmul_bias_relu(a, b, bias))
+    for _ in range(3):
+        out.fill_(float("nan"))
+        ex.launch()
+        torch.cuda.synchronize()
+        assert np.array_equal(out.float().cpu().numpy().astype(np.float64), want)
+
+
 @pytest.mark.parametrize("bn", [128, 256])
 def test_lean_drain_residual_exact(bn):
     """D = relu(A B + bias) + R with a bf16 residual (the FFN's second GEMM form)."""
