@@ -839,7 +839,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
       // drained by: the group's 4 warps, or all 8 when the groups split columns (of both CTAs)
-      ptx::mbar_init(&tempty[a], (!GENERIC || p.epi_fast ? 8 : 4) * CG);
+      ptx::mbar_init(&tempty[a], ((!GENERIC || p.epi_fast) && (CG == 1 || p.split_k == 1) ? 8 : 4) * CG);
     }
     ptx::fence_mbar_init();
   }
@@ -1189,7 +1189,9 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
       }
     };
     uint32_t nvalid = 0;
-    const bool colsplit = !GENERIC || p.epi_fast;
+    // (CTA-pair split-K keeps the one-group-per-unit path: the lean split form hung in
+    // back-to-back launches of the CG=2 FFN chain, scripts/space_probe.py config 56)
+    const bool colsplit = (!GENERIC || p.epi_fast) && (CG == 1 || p.split_k == 1);
     uint32_t acc_phase2[2] = {0u, 0u};  // colsplit: per-buffer phase
     // canonical S / T of columns gt and gt + 128 of tile column block tn_ (batch b_)
     auto fetch_st = [&](int tn_, int b_, float (&s_v)[2], float (&t_v)[2]) {
@@ -1321,7 +1323,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
       const uint32_t taddr = tmem_base + (static_cast<uint32_t>(lg * 32) << 16) + abuf * BN;
       if (lead) detail::trace(p, i, TR_EPI_ACC, t0);
       const int ncols = static_cast<int>(min(static_cast<int64_t>(BN), p.N - n0));  // valid columns
-      if (p.split_k > 1 && colsplit) {
+      if (CG == 1 && p.split_k > 1 && colsplit) {
         // ---- split-K, lean form: each group parks its column half of the raw partial
         // tile; the group that completes a (tile, half) last reduces it and stores
         constexpr int kHalf = BN / 2;
