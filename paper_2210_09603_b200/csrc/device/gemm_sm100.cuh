@@ -690,20 +690,29 @@ __device__ __forceinline__ void drain_reduce(const CUtensorMap* tmC, const float
     float x[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) x[j] = 0.f;
+    // the workspace round trip is an L2 latency (~1-2k clk under load): issue
+    // every split of a 16-column half-chunk before adding (up to 4 splits per
+    // batch), then add in split order (deterministic)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
 #pragma unroll 1
-    for (int sp = 0; sp < split_k; ++sp) {  // fixed order: deterministic
-      const float* base = ws + static_cast<int64_t>(sp) * (kBM * BN);
-      float4 f[8];
+      for (int sp0 = 0; sp0 < split_k; sp0 += 4) {
+        float4 f[4][4];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const float4* src = reinterpret_cast<const float4*>(
-            base + (static_cast<int64_t>((cofs + c) / 16 + h) * kBM + rloc) * 16);
+        for (int u = 0; u < 4; ++u) {
+          const float4* src = reinterpret_cast<const float4*>(
+              ws + static_cast<int64_t>(min(sp0 + u, split_k - 1)) * (kBM * BN) +
+              (static_cast<int64_t>((cofs + c) / 16 + h) * kBM + rloc) * 16);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) f[4 * h + q] = __ldcg(src + q);
-      }
+          for (int q = 0; q < 4; ++q) f[u][q] = sp0 + u < split_k ? __ldcg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        x[4 * q] += f[q].x; x[4 * q + 1] += f[q].y; x[4 * q + 2] += f[q].z; x[4 * q + 3] += f[q].w;
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            x[16 * h + 4 * q] += f[u][q].x; x[16 * h + 4 * q + 1] += f[u][q].y;
+            x[16 * h + 4 * q + 2] += f[u][q].z; x[16 * h + 4 * q + 3] += f[u][q].w;
+          }
       }
     }
     uint4 rq[4];
@@ -1348,10 +1357,13 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
           }
         }
         release_acc(abuf);  // TMEM is free again: the MMA can start the next unit
+        if (lead) detail::trace(p, i, 8, t0);
         __threadfence();
+        if (lead) detail::trace(p, i, 9, t0);
         ptx::named_bar_sync(3 + grp, 128);
         if (gt == 0) split_flag[grp] = (atomicAdd(&p.counters[tile_id * 2 + grp], 1) == p.split_k - 1) ? 1u : 0u;
         ptx::named_bar_sync(3 + grp, 128);
+        if (lead) detail::trace(p, i, 10, t0);
         if (*reinterpret_cast<volatile uint32_t*>(&split_flag[grp]) == 0u) continue;
         __threadfence();
         const uint4* res = nullptr;
@@ -1370,6 +1382,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
           default: __trap();
         }
         if (gt == 0) p.counters[tile_id * 2 + grp] = 0;  // self-resetting for the next launch
+        if (lead) detail::trace(p, i, 11, t0);
         continue;
       }
       if (p.split_k > 1) {

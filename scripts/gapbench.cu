@@ -15,6 +15,10 @@ template <bool TMEM>
 __global__ void k_empty(Big p, unsigned long long* t) {
   extern __shared__ unsigned char sm[];
   __shared__ unsigned slot;
+  if (p.b[1] == 1) {  // PDL variant
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+  }
   if (TMEM) {
     if (threadIdx.x < 32) {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(
@@ -40,19 +44,34 @@ int main() {
     const char* name;
     bool tmem;
     int smem, threads;
-  } vs[] = {{"empty 128 thr", false, 0, 128},
-            {"empty 416 thr", false, 0, 416},
-            {"+200KB smem", false, smem_big, 416},
-            {"+TMEM alloc", true, smem_big, 416},
-            {"TMEM no smem", true, 0, 416}};
+    bool pdl;
+  } vs[] = {{"empty 128 thr", false, 0, 128, false},
+            {"empty 416 thr", false, 0, 416, false},
+            {"+200KB smem", false, smem_big, 416, false},
+            {"+TMEM alloc", true, smem_big, 416, false},
+            {"TMEM no smem", true, 0, 416, false},
+            {"PDL empty 128", false, 0, 128, true},
+            {"PDL +200KB+TMEM", true, smem_big, 416, true},
+            {"PDL 200KB+TMEM 384", true, smem_big, 384, true}};
   for (auto& v : vs) {
     const int n = 50;
     cudaGraph_t g;
     cudaGraphExec_t ge;
     cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal);
+    p.b[1] = v.pdl ? 1 : 0;
     for (int i = 0; i < n; ++i) {
-      if (v.tmem) k_empty<true><<<148, v.threads, v.smem, s>>>(p, t);
-      else k_empty<false><<<148, v.threads, v.smem, s>>>(p, t);
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(148);
+      cfg.blockDim = dim3(v.threads);
+      cfg.dynamicSmemBytes = v.smem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      at[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = v.pdl ? 1 : 0;
+      if (v.tmem) cudaLaunchKernelEx(&cfg, k_empty<true>, p, t);
+      else cudaLaunchKernelEx(&cfg, k_empty<false>, p, t);
     }
     cudaStreamEndCapture(s, &g);
     cudaGraphInstantiate(&ge, g, 0);
