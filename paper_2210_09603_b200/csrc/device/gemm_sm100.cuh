@@ -681,7 +681,8 @@ __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t tadd
 template <int BN, int CG, int OUT_ROW, int ACT, bool RES>
 __device__ __forceinline__ void drain_reduce(const CUtensorMap* tmC, const float* ws, int split_k, int rloc,
                                              int cofs, const float* colbuf, uint8_t* obuf, int ncols,
-                                             int32_t col_base, int32_t row0, int32_t b, int lane, const uint4* res) {
+                                             int32_t col_base, int32_t row0, int32_t b, int lane, const uint4* res,
+                                             long long* tk = nullptr, long long t0 = 0) {
   constexpr int GC = OUT_ROW / 2;
   uint8_t* const orow = obuf + lane * OUT_ROW;
   const int swz = OUT_ROW == 128 ? (lane & 7) : ((lane >> 1) & 3);
@@ -715,6 +716,7 @@ __device__ __forceinline__ void drain_reduce(const CUtensorMap* tmC, const float
           }
       }
     }
+    if (tk != nullptr && c == 0 && lane == 0) tk[12] = clock64() - t0 + (static_cast<long long>(__float_as_int(x[0]) & 0) );
     uint4 rq[4];
     if constexpr (RES) {
 #pragma unroll
@@ -759,6 +761,7 @@ __device__ __forceinline__ void drain_reduce(const CUtensorMap* tmC, const float
         ptx::bulk_commit();
       }
     }
+    if (tk != nullptr && c == 0 && lane == 0) tk[13] = clock64() - t0;
   }
 }
 
@@ -1371,11 +1374,15 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
           res = reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(p.ops[p.canon_res_op].ptr) +
                                                detail::addr_rowpart(p.ops[p.canon_res_op].a, rr, b) + n0 + cofs);
         const int32_t cbase = static_cast<int32_t>(n0) + cofs;
+        long long* tk = (p.trace != nullptr && e == 0 && i < static_cast<uint32_t>(kTraceTiles))
+                            ? p.trace + (static_cast<int64_t>(blockIdx.x) * kTraceTiles + i) * kTraceEvents
+                            : nullptr;
+        if (tk != nullptr && lane == 0) tk[7] = clock64() - t0;  // reduce start (after the fence)
         switch (p.canon_act * 2 + (p.canon_res_op >= 0 ? 1 : 0)) {
 #define TMB_RED(A, R)                                                                                              \
   case A * 2 + R:                                                                                                  \
     detail::drain_reduce<BN, CG, Cfg::OUT_ROW, A, R>(&tmC, ws, p.split_k, rloc, cofs, colbuf + cofs, obuf, hcols,  \
-                                                     cbase, row0, b, lane, res);                                   \
+                                                     cbase, row0, b, lane, res, tk, t0);                           \
     break;
           TMB_RED(0, 0) TMB_RED(0, 1) TMB_RED(1, 0) TMB_RED(1, 1) TMB_RED(2, 0) TMB_RED(2, 1)
 #undef TMB_RED
