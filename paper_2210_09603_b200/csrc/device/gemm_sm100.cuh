@@ -701,11 +701,12 @@ __device__ __forceinline__ void drain_reduce(const CUtensorMap* tmC, const float
         float4 f[4][4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const float4* src = reinterpret_cast<const float4*>(
-              ws + static_cast<int64_t>(min(sp0 + u, split_k - 1)) * (kBM * BN) +
-              (static_cast<int64_t>((cofs + c) / 16 + h) * kBM + rloc) * 16);
+          const float4* src = reinterpret_cast<const float4*>(ws + static_cast<int64_t>(min(sp0 + u, split_k - 1)) *
+                                                                         (kBM * BN)) +
+                              (static_cast<int64_t>((cofs + c) / 4 + 4 * h) * kBM + rloc);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) f[u][q] = sp0 + u < split_k ? __ldcg(src + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int q = 0; q < 4; ++q)
+            f[u][q] = sp0 + u < split_k ? __ldcg(src + q * kBM) : make_float4(0.f, 0.f, 0.f, 0.f);
         }
 #pragma unroll
         for (int u = 0; u < 4; ++u)
@@ -1349,14 +1350,18 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
           uint32_t r[32];
           ptx::tmem_ld32(taddr + cofs + c, r);
           ptx::tmem_wait_ld();
+          // layout [split][col/4][128 rows] of float4: each store instruction of a
+          // warp writes 512 contiguous bytes (whole lines), and the reader uses the
+          // same lane -> row mapping
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            float4* dst = reinterpret_cast<float4*>(const_cast<float*>(ws) + ks * static_cast<int64_t>(kBM * BN) +
-                                                    (static_cast<int64_t>((cofs + c) / 16 + h) * kBM + rloc) * 16);
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              __stcg(dst + q, make_float4(__uint_as_float(r[16 * h + 4 * q]), __uint_as_float(r[16 * h + 4 * q + 1]),
-                                          __uint_as_float(r[16 * h + 4 * q + 2]), __uint_as_float(r[16 * h + 4 * q + 3])));
+            for (int q = 0; q < 4; ++q) {
+              float4* dst = reinterpret_cast<float4*>(const_cast<float*>(ws) + ks * static_cast<int64_t>(kBM * BN)) +
+                            (static_cast<int64_t>((cofs + c) / 4 + 4 * h + q) * kBM + rloc);
+              __stcg(dst, make_float4(__uint_as_float(r[16 * h + 4 * q]), __uint_as_float(r[16 * h + 4 * q + 1]),
+                                      __uint_as_float(r[16 * h + 4 * q + 2]), __uint_as_float(r[16 * h + 4 * q + 3])));
+            }
           }
         }
         release_acc(abuf);  // TMEM is free again: the MMA can start the next unit
