@@ -920,7 +920,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
     };
     // SM-pair (cta_group::2, 256-row tiles) when requested and every operand is TMA-fed
     k.cg = 1;
-    if (!k.simt && plan.cfg.block_m == 256 && (k.bn == 128 || k.bn == 256) && bind_operands(2)) k.cg = 2;
+    if (!k.simt && plan.cfg.block_m == 256 && (k.bn == 64 || k.bn == 128 || k.bn == 256) && bind_operands(2)) k.cg = 2;
     else bind_operands(1);
     p.tiles_m = static_cast<int32_t>((sp.M + 128 * k.cg - 1) / (128 * k.cg));
     if (k.simt) {

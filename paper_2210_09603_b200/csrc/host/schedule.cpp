@@ -72,7 +72,7 @@ std::vector<ScheduleConfig> schedule_space(const std::string& op_kind) {
           out.push_back(c);
         }
   // SM-pair tiles (256 x N, tcgen05.mma.cta_group::2), deep ring
-  for (int bn : {256, 128})
+  for (int bn : {256, 128, 64})
     for (int sk : {1, 2, 4})
       for (int raster : {0, 1}) {
         ScheduleConfig c;

@@ -10,7 +10,7 @@ bool launch_cg2(const BoundKernel& k, cudaStream_t s) {
     else if (k.generic) launch_one<BN, stages_for(BN, 2), false, 2, true>(k, s);  \
     else launch_one<BN, stages_for(BN, 2, false), false, 2, false>(k, s);                \
     return true;
-    TMB_V(128) TMB_V(256)
+    TMB_V(64) TMB_V(128) TMB_V(256)
 #undef TMB_V
   }
   return false;

@@ -29,7 +29,7 @@ def _matmul_case(m, n, k, exact, seed):
     return a, b, bias
 
 
-@pytest.mark.parametrize("bm,bn", [(128, 64), (128, 128), (128, 192), (128, 256), (256, 128), (256, 256)])
+@pytest.mark.parametrize("bm,bn", [(128, 64), (128, 128), (128, 192), (128, 256), (256, 64), (256, 128), (256, 256)])
 @pytest.mark.parametrize("b_layout", [None, "t"])  # B[K,N] MN-major (TMA MN) / K-major storage
 def test_matmul_bias_relu_exact(bm, bn, b_layout):
     """block_m=256 runs the SM-pair form (tcgen05.mma.cta_group::2)."""
@@ -106,7 +106,7 @@ def test_matmul_bf16_output():
     assert port.max_rel_error(got["D"], port.matmul_bias_relu(a, b, rounded(bias, "bf16"))) <= 1e-2
 
 
-@pytest.mark.parametrize("bm,bn", [(128, 64), (128, 128), (128, 192), (128, 256), (256, 128), (256, 256)])
+@pytest.mark.parametrize("bm,bn", [(128, 64), (128, 128), (128, 192), (128, 256), (256, 64), (256, 128), (256, 256)])
 @pytest.mark.parametrize("mn", [(333, 200), (640, 520)])
 def test_lean_drain_bf16_output_exact(bm, bn, mn):
     """bf16 TMA-stored output + canonical epilogue: the lean drain path, the two
