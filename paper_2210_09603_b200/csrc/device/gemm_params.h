@@ -163,6 +163,9 @@ struct GemmParams {
   // ring slot: B is loaded in the first ring pass only and stays resident
   int32_t b_resident;
   int32_t ring;  // ring slots in use (0 = all STAGES)
+  // MN-major B as one 4-D box {64 n, BK k, BN/64 n-blocks} per slot instead of
+  // BN/64 boxes (TMA issue is ~600 clk per box per warp): needs N % 64 == 0
+  int32_t b_mn4d;
   // lean drain writes bf16 rows straight from registers (16-byte stores) instead
   // of smem staging + TMA store: row-major output, 16-byte aligned rows, N % 8 == 0
   int32_t out_direct;

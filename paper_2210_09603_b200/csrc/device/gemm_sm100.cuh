@@ -969,9 +969,13 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
                   if (p.b_loader == LD_TMA_K) {
                     ptx::tma_load_3d_2sm(b_tile, &tmB, lead_full, k0, n0, b);
                   } else {
+                    if (p.b_mn4d) {
+                      ptx::tma_load_4d_2sm(b_tile, &tmB, lead_full, 0, k0, n0 / 64, b);
+                    } else {
 #pragma unroll 1
-                    for (int j = 0; j < BN / CG / 64; ++j)
-                      ptx::tma_load_3d_2sm(b_tile + j * (64 * kRowBytes), &tmB, lead_full, n0 + 64 * j, k0, b);
+                      for (int j = 0; j < BN / CG / 64; ++j)
+                        ptx::tma_load_3d_2sm(b_tile + j * (64 * kRowBytes), &tmB, lead_full, n0 + 64 * j, k0, b);
+                    }
                   }
                 }
               } else {
@@ -1015,9 +1019,13 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
                   if (p.b_loader == LD_TMA_K) {
                     ptx::tma_load_3d(b_tile, &tmB, &full[stage], k0, n0, b);
                   } else {
+                    if (p.b_mn4d) {
+                      ptx::tma_load_4d(b_tile, &tmB, &full[stage], 0, k0, n0 / 64, b);
+                    } else {
 #pragma unroll 1
-                    for (int j = 0; j < BN / 64; ++j)
-                      ptx::tma_load_3d(b_tile + j * (64 * kRowBytes), &tmB, &full[stage], n0 + 64 * j, k0, b);
+                      for (int j = 0; j < BN / 64; ++j)
+                        ptx::tma_load_3d(b_tile + j * (64 * kRowBytes), &tmB, &full[stage], n0 + 64 * j, k0, b);
+                    }
                   }
                 }
               }
@@ -1074,10 +1082,14 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
             } else if (p.b_loader == LD_TMA_K) {
               ptx::tma_load_3d(b_tile, &tmB, &full[stage], k0, n0, b);
             } else if (p.b_loader == LD_TMA_MN) {
+              if (p.b_mn4d) {
+                ptx::tma_load_4d(b_tile, &tmB, &full[stage], 0, k0, n0 / 64, b);
+              } else {
 #pragma unroll 1
-              for (int j = 0; j < BN / 64; ++j)
-                ptx::tma_load_3d(b_tile + j * (64 * kRowBytes), &tmB, &full[stage], n0 + 64 * j,
-                                 k0, b);
+                for (int j = 0; j < BN / 64; ++j)
+                  ptx::tma_load_3d(b_tile + j * (64 * kRowBytes), &tmB, &full[stage], n0 + 64 * j,
+                                   k0, b);
+              }
             }
           }
           if (GENERIC && !all_tma) {

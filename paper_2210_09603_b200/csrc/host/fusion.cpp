@@ -906,10 +906,22 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
         make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * esize(opb->dtype), opb->dtype, 3, dims, strides, box);
       } else if (!k.tf32 && bn_cta % 64 == 0 && tma_ok_mnmajor(f, *opb, sp.N)) {
         p.b_loader = LD_TMA_MN;
-        const uint64_t dims[3] = {(uint64_t)sp.N, (uint64_t)sp.K, (uint64_t)sp.batch};
-        const uint64_t strides[2] = {(uint64_t)(f.c1 * 2), (uint64_t)(std::max<int64_t>(f.c2, f.c1 * sp.K) * 2)};
-        const uint32_t box[3] = {64u, (uint32_t)BK, 1u};
-        make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * 2, opb->dtype, 3, dims, strides, box);
+        if (sp.N % 64 == 0 && !std::getenv("TMB_NO_MN4D")) {
+          // {64 n, K, N/64 n-blocks, batch}: one box per slot lands the BN/64 column
+          // blocks at 8 KB strides, the layout the per-block boxes produced
+          p.b_mn4d = 1;
+          const uint64_t dims[4] = {64, (uint64_t)sp.K, (uint64_t)(sp.N / 64), (uint64_t)sp.batch};
+          const uint64_t strides[3] = {(uint64_t)(f.c1 * 2), 128,
+                                       (uint64_t)(std::max<int64_t>(f.c2, f.c1 * sp.K) * 2)};
+          const uint32_t box[4] = {64u, (uint32_t)BK, (uint32_t)(bn_cta / 64), 1u};
+          make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * 2, opb->dtype, 4, dims, strides, box);
+        } else {
+          p.b_mn4d = 0;
+          const uint64_t dims[3] = {(uint64_t)sp.N, (uint64_t)sp.K, (uint64_t)sp.batch};
+          const uint64_t strides[2] = {(uint64_t)(f.c1 * 2), (uint64_t)(std::max<int64_t>(f.c2, f.c1 * sp.K) * 2)};
+          const uint32_t box[3] = {64u, (uint32_t)BK, 1u};
+          make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * 2, opb->dtype, 3, dims, strides, box);
+        }
       } else {
         p.b_loader = LD_GATHER;
       }
