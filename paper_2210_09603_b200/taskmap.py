@@ -543,9 +543,10 @@ class Graph:
 class Plan:
     """partition + fuse + schedule a DAG onto the sm_100a tensor programs (tm_plan)."""
 
-    def __init__(self, dag: ComputeDAG, config: Optional[ScheduleConfig] = None, device: int = 0):
+    def __init__(self, dag: ComputeDAG, config: Optional[ScheduleConfig] = None, device: Optional[int] = None):
         self.dag = dag
         self.config = config or ScheduleConfig()
+        device = _resolve_device(device)
         c = self.config.to_c()
         h = ctypes.c_void_p()
         _check(load_library().tm_plan_create(dag.to_json().encode(), ctypes.byref(c), int(device), ctypes.byref(h)))
@@ -570,8 +571,27 @@ class Plan:
             self._h = None
 
 
-def tune(dag: ComputeDAG, inputs, outputs, device: int = 0, reps: int = 5):
+def _resolve_device(device: Optional[int], tensors=()) -> int:
+    """The CUDA device a plan binds / tunes on: explicit, else that of the first
+    CUDA tensor given, else torch's current device (one process per GPU: rank r
+    must not fall back to device 0)."""
+    if device is not None:
+        return int(device)
+    for t in tensors:
+        if getattr(t, "is_cuda", False):
+            return int(t.device.index)
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return int(torch.cuda.current_device())
+    except Exception:  # noqa: BLE001
+        pass
+    return 0
+
+
+def tune(dag: ComputeDAG, inputs, outputs, device: Optional[int] = None, reps: int = 5):
     """Exhaustive on-device tuning over schedule_space; returns (best, report)."""
+    device = _resolve_device(device, list(inputs) + list(outputs))
     ins = (TmTensor * max(1, len(inputs)))(*[_tensor_arg(t) for t in inputs])
     outs = (TmTensor * max(1, len(outputs)))(*[_tensor_arg(t) for t in outputs])
     best = TmScheduleConfig()

@@ -64,3 +64,19 @@ def test_gloo_two_rank_sharded_gather():
         p.join(100)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=5) is True
+
+
+def test_plan_device_follows_the_process_gpu():
+    """One process per GPU: a plan bound by rank r must target cuda:r, not device 0
+    (tm_exec_create switches to the plan's device before allocating scratch)."""
+    from paper_2210_09603_b200.taskmap import _resolve_device
+
+    class FakeCuda:
+        is_cuda = True
+
+        class device:  # noqa: N801
+            index = 5
+
+    assert _resolve_device(2) == 2
+    assert _resolve_device(None, [object(), FakeCuda()]) == 5
+    assert isinstance(_resolve_device(None), int)
