@@ -1576,9 +1576,13 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
           if (kb == kb0 && lane == 0) detail::trace(p, i, TR_MMA_FIRST, t0);
           const uint64_t ad = adesc0 + static_cast<uint64_t>((stage * Cfg::A_BYTES) >> 4);
           const uint64_t bd = bdesc0 + static_cast<uint64_t>((stage * Cfg::B_BYTES) >> 4);
+          // K16 steps wholly past K (the last k-block of a ragged K, e.g. conv1's
+          // 49 taps) multiply zero-filled operands: skip them
+          const int ksteps = min(Cfg::NSTEP, (p.K - kb * BK + Cfg::KSTEP - 1) / Cfg::KSTEP);
           if (ptx::elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < Cfg::NSTEP; ++kk) {
+              if (kk > 0 && kk >= ksteps) break;
               const uint64_t adesc = ad + static_cast<uint64_t>(kk * a_kstep);
               const uint64_t bdesc = bd + static_cast<uint64_t>(kk * b_kstep);
               const uint32_t accum = (kb != kb0 || kk != 0);
