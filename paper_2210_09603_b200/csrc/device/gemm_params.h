@@ -63,7 +63,7 @@ constexpr int kTraceEvents = 16;  // 0-7 role events (TraceEv); tile 0: 14/15 = 
 // kernel), so BN/2 must be a whole number of store groups: 64-byte rows
 // (32 bf16 columns) for BN = 64 and 192.
 constexpr int out_stage_row_bytes(int bn, int cg) {
-  return ((bn == 256 && cg == 1) || bn == 64 || bn == 192) ? 64 : 128;
+  return ((bn == 256 && cg == 1) || bn == 64 || bn == 96 || bn == 192) ? 64 : 128;
 }
 // trace events per tile
 enum TraceEv : int32_t {

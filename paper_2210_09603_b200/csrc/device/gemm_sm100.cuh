@@ -852,7 +852,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
       // drained by: the group's 4 warps, or all 8 when the groups split columns (of both CTAs)
-      ptx::mbar_init(&tempty[a], ((!GENERIC || p.epi_fast) && (CG == 1 || p.split_k == 1) ? 8 : 4) * CG);
+      ptx::mbar_init(&tempty[a], ((!GENERIC || p.epi_fast) && (CG == 1 || p.split_k == 1) && BN % 64 == 0 ? 8 : 4) * CG);
     }
     ptx::fence_mbar_init();
   }
@@ -1216,7 +1216,11 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
     uint32_t nvalid = 0;
     // (CTA-pair split-K keeps the one-group-per-unit path: the lean split form hung in
     // back-to-back launches of the CG=2 FFN chain, scripts/space_probe.py config 56)
-    const bool colsplit = (!GENERIC || p.epi_fast) && (CG == 1 || p.split_k == 1);
+    // lean drain (drain_fast) for canonical bf16 epilogues; the two groups split each
+    // tile's columns when the halves are whole 32-column chunks (BN % 64 == 0),
+    // otherwise they alternate tiles, full width
+    const bool lean = !GENERIC || p.epi_fast;
+    const bool colsplit = lean && (CG == 1 || p.split_k == 1) && BN % 64 == 0;
     uint32_t acc_phase2[2] = {0u, 0u};  // colsplit: per-buffer phase
     // canonical S / T of columns gt and gt + 128 of tile column block tn_ (batch b_)
     auto fetch_st = [&](int tn_, int b_, float (&s_v)[2], float (&t_v)[2]) {
@@ -1460,12 +1464,12 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
       }
       // 32 columns per TMEM load; the accumulator is released right after the
       // last load, before the math of the last columns
-      if (colsplit) {
+      if (lean) {
         // lean drain (host guarantees via epi_fast: canonical epilogue, bf16 TMA-stored
         // output, residual absent or bf16 contiguous 16-byte aligned with N % 32 == 0)
         // this group's column half of the tile
-        constexpr int kHalf = BN / 2;
-        const int cofs = grp * kHalf;
+        const int kHalf = colsplit ? BN / 2 : BN;
+        const int cofs = colsplit ? grp * kHalf : 0;
         const int hcols = max(0, min(kHalf, ncols - cofs));
         const uint4* res = nullptr;
         if (p.canon_res_op >= 0)

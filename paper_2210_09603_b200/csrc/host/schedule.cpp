@@ -59,7 +59,7 @@ std::vector<ScheduleConfig> schedule_space(const std::string& op_kind) {
     fail("unknown op kind '", op_kind, "' for schedule_space");
   std::vector<ScheduleConfig> out;
   // single-SM tiles (128 x N): every N, double buffer or deep ring, split-K
-  for (int bn : {128, 256, 192, 64})
+  for (int bn : {128, 256, 192, 64, 96})
     for (int sk : {1, 2, 4})
       for (bool deep : {true, false})
         for (int raster : {0, 1}) {

@@ -7,7 +7,7 @@ bool launch_cg1_generic_bf16(const BoundKernel& k, cudaStream_t s) {
   switch (k.bn) {
 #define TMB_V(BN) \
   case BN: if (deep) launch_one<BN, stages_for(BN, 1, true), false, 1, true>(k, s); else launch_one<BN, 2, false, 1, true>(k, s); return true;
-    TMB_V(64) TMB_V(128) TMB_V(192) TMB_V(256)
+    TMB_V(64) TMB_V(96) TMB_V(128) TMB_V(192) TMB_V(256)
 #undef TMB_V
   }
   return false;

@@ -29,7 +29,8 @@ def _matmul_case(m, n, k, exact, seed):
     return a, b, bias
 
 
-@pytest.mark.parametrize("bm,bn", [(128, 64), (128, 128), (128, 192), (128, 256), (256, 64), (256, 128), (256, 256)])
+@pytest.mark.parametrize("bm,bn", [(128, 64), (128, 96), (128, 128), (128, 192), (128, 256), (256, 64), (256, 128),
+                                   (256, 256)])
 @pytest.mark.parametrize("b_layout", [None, "t"])  # B[K,N] MN-major (TMA MN) / K-major storage
 def test_matmul_bias_relu_exact(bm, bn, b_layout):
     """block_m=256 runs the SM-pair form (tcgen05.mma.cta_group::2)."""
@@ -106,7 +107,8 @@ def test_matmul_bf16_output():
     assert port.max_rel_error(got["D"], port.matmul_bias_relu(a, b, rounded(bias, "bf16"))) <= 1e-2
 
 
-@pytest.mark.parametrize("bm,bn", [(128, 64), (128, 128), (128, 192), (128, 256), (256, 64), (256, 128), (256, 256)])
+@pytest.mark.parametrize("bm,bn", [(128, 64), (128, 96), (128, 128), (128, 192), (128, 256), (256, 64), (256, 128),
+                                   (256, 256)])
 @pytest.mark.parametrize("mn", [(333, 200), (640, 520)])
 def test_lean_drain_bf16_output_exact(bm, bn, mn):
     """bf16 TMA-stored output + canonical epilogue: the lean drain path, the two
@@ -122,7 +124,8 @@ def test_lean_drain_bf16_output_exact(bm, bn, mn):
     assert np.array_equal(got["D"], port.round_bf16(port.matmul_bias_relu(a, b, bias)))
 
 
-@pytest.mark.parametrize("bm,bn,split_k", [(128, 128, 2), (128, 256, 3), (256, 128, 2), (128, 64, 4), (128, 192, 3)])
+@pytest.mark.parametrize("bm,bn,split_k", [(128, 128, 2), (128, 256, 3), (256, 128, 2), (128, 64, 4), (128, 192, 3),
+                                           (128, 96, 2)])
 def test_lean_split_k_bf16_exact(bm, bn, split_k):
     """Split-K with the lean drain: each epilogue group parks its column half of the
     partial tile, the last arriver of each (tile, half) reduces in split order and
