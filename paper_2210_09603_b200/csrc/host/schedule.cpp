@@ -59,10 +59,15 @@ std::vector<ScheduleConfig> schedule_space(const std::string& op_kind) {
     fail("unknown op kind '", op_kind, "' for schedule_space");
   std::vector<ScheduleConfig> out;
   // single-SM tiles (128 x N): every N, double buffer or deep ring, split-K
-  for (int bn : {128, 256, 192, 64, 96})
-    for (int sk : {1, 2, 4})
+  // Kept out of the tuned space (instantiated and parity-tested): split-K 4, and
+  // split-K with BN=64 -- back-to-back launches of the BERT FFN chain under
+  // those hung intermittently on the GPU box (scripts/space_probe.py, ~1 in 3
+  // sweeps of the space); not yet root-caused.
+  for (int bn : {128, 256, 192, 64})
+    for (int sk : {1, 2})
       for (bool deep : {true, false})
         for (int raster : {0, 1}) {
+          if (bn == 64 && sk > 1) continue;
           ScheduleConfig c;
           c.block_n = bn;
           c.split_k = sk;
@@ -71,10 +76,43 @@ std::vector<ScheduleConfig> schedule_space(const std::string& op_kind) {
           c.raster = raster;
           out.push_back(c);
         }
+  // BN=96 tiles (147 tiles for the 6272-pixel ResNet stage-3 maps at F=256), no split
+  for (bool deep : {true, false})
+    for (int raster : {0, 1}) {
+      ScheduleConfig c;
+      c.block_n = 96;
+      c.pipeline = deep;
+      c.stages = deep ? 0 : 2;
+      c.raster = raster;
+      out.push_back(c);
+    }
+  // half-size persistent grids (74 CTAs, two SMs' worth of tiles each): L2 reuse
+  // across a CTA's consecutive tiles against fewer SMs in flight
+  for (int bn : {128, 256, 192, 64, 96})
+    for (int raster : {0, 1}) {
+      ScheduleConfig c;
+      c.block_n = bn;
+      c.raster = raster;
+      c.grid = 74;
+      out.push_back(c);
+    }
+  for (int bn : {128, 256})
+    for (int raster : {0, 1}) {
+      ScheduleConfig c;
+      c.block_n = bn;
+      c.pipeline = false;
+      c.stages = 2;
+      c.raster = raster;
+      c.grid = 74;
+      out.push_back(c);
+    }
   // SM-pair tiles (256 x N, tcgen05.mma.cta_group::2), deep ring
-  for (int bn : {256, 128, 64})
-    for (int sk : {1, 2, 4})
+  // (BN=128 pairs are instantiated and parity-tested but not tuned: back-to-back
+  // launches of the GELU/residual FFN chain with them hung on the GPU box)
+  for (int bn : {256, 64})
+    for (int sk : {1, 2})
       for (int raster : {0, 1}) {
+        if (bn == 64 && sk > 1) continue;
         ScheduleConfig c;
         c.block_m = 256;
         c.block_n = bn;

@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "../device/gemm_sm100.cuh"
@@ -35,9 +36,12 @@ void launch_one(const BoundKernel& k, cudaStream_t s) {
   int na = 0;
   // programmatic dependent launch: this grid's prologue overlaps the previous
   // kernel's tail (the kernel waits with griddepcontrol.wait before touching memory)
-  attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[na].val.programmaticStreamSerializationAllowed = 1;
-  ++na;
+  static const bool pdl = std::getenv("TMB_NO_PDL") == nullptr;
+  if (pdl) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   if constexpr (CG == 2) {
     attr[na].id = cudaLaunchAttributeClusterDimension;
     attr[na].val.clusterDim.x = CG;

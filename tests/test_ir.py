@@ -113,7 +113,7 @@ def test_schedule_space_size_and_agnostic():
     s = schedule_space("matmul")
     assert 50 <= len(s) <= 200
     assert s == schedule_space("conv2d")
-    assert len({(c.block_m, c.block_n, c.split_k, c.pipeline, c.raster) for c in s}) == len(s)
+    assert len({(c.block_m, c.block_n, c.split_k, c.pipeline, c.raster, c.grid) for c in s}) == len(s)
 
 
 def test_unsupported_reports_unsupported_status():
