@@ -7,7 +7,7 @@ OUT=gpurun_out/$TAG; rm -rf $OUT; mkdir -p $OUT
 nvidia-smi > $OUT/nvidia-smi.txt 2>&1
 timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest exit $?" >> $OUT/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke exit $?" >> $OUT/smoke.log
-timeout 1200 python bench.py --per-item --tune force > $OUT/bench.json 2> $OUT/bench.err
+timeout 1200 python bench.py --per-item > $OUT/bench.json 2> $OUT/bench.err
 cp tuning_cache.json $OUT/tuning_cache.json
 timeout 900 python bench.py > $OUT/bench2.json 2> $OUT/bench2.err
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > $OUT/bench_ref.json 2> $OUT/bench_ref.err
