@@ -33,6 +33,33 @@ template <class... Args>
   throw Error(os.str());
 }
 
+// Typed refinements of Error for the C ABI's status codes (tm_status): the
+// boundary maps the exception type, never the message text, to a code.
+struct UnsupportedError : Error {  // TM_ERR_UNSUPPORTED: valid input outside what the device path implements
+  using Error::Error;
+};
+struct CudaError : Error {  // TM_ERR_CUDA: a CUDA runtime / driver call failed
+  using Error::Error;
+};
+struct CorrectnessError : Error {  // TM_ERR_CORRECTNESS: a result failed its correctness gate
+  using Error::Error;
+};
+
+template <class E, class... Args>
+[[noreturn]] void fail_as(Args&&... args) {
+  std::ostringstream os;
+  (os << ... << args);
+  throw E(os.str());
+}
+template <class... Args>
+[[noreturn]] void fail_unsupported(Args&&... args) {
+  fail_as<UnsupportedError>(std::forward<Args>(args)...);
+}
+template <class... Args>
+[[noreturn]] void fail_cuda(Args&&... args) {
+  fail_as<CudaError>(std::forward<Args>(args)...);
+}
+
 enum class DType { F32, I32 };
 const char* dtype_name(DType t);
 DType dtype_from_name(const std::string& s);

@@ -136,12 +136,25 @@ tm_status tm_graph_launch(const tm_graph* g, void* cuda_stream);
 tm_status tm_graph_exec_ms(const tm_graph* g, float* ms, int32_t n);
 void tm_graph_destroy(tm_graph* g);
 
-/* tune: enumerate the space on the bound tensors, time each
- * config with CUDA events, gate on agreement with the default config, pick
- * the fastest (ties: space order). Report JSON (TuneReport). */
+/* tune: enumerate schedule_space; verify every config on two
+ * fixed seeded inputs (integer U{-8..8}: bit-exact where the DAG keeps integers
+ * exact; dyadic k/256: within tolerance) against the device DAG interpreter
+ * (tm_dag_eval); time the config on the bound tensors with CUDA events; pick
+ * the fastest correct one (ties: space order).  Correctness is a hard gate: any
+ * incorrect config aborts with TM_ERR_CORRECTNESS.  The TuneReport JSON
+ * is returned through *report_json in both cases. */
 tm_status tm_tune(const char* dag_json, const tm_tensor* inputs, int32_t n_in,
                   const tm_tensor* outputs, int32_t n_out, int32_t device, int32_t reps,
                   tm_schedule_config* best, char** report_json);
+
+/* reference_eval (proj/include/taskmap/compute_ir.hpp:60) re-run on the device:
+ * every node of the DAG evaluated element by element with the reference
+ * interpreter's semantics (fp64 / int64 values, row-major reductions from the
+ * combiner identity, short-circuit select).  Independent of the tensor
+ * programs; it is the tuner's correctness reference.  Outputs are written
+ * rounded to their dtype; synchronous on `cuda_stream`. */
+tm_status tm_dag_eval(const char* dag_json, const tm_tensor* inputs, int32_t n_in,
+                      const tm_tensor* outputs, int32_t n_out, int32_t device, void* cuda_stream);
 
 #ifdef __cplusplus
 }

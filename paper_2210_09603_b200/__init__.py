@@ -12,7 +12,7 @@ from .taskmap import (  # noqa: F401
     land, lor, lt, le, gt, ge, eq, ne, neg, relu, exp, sqrt, gelu_tanh, zero_of,
     Axis, TensorNode, ComputeDAG, classify, partition,
     matmul_dag, conv2d_im2col_dag, batchnorm_inference_dag, transpose_dag, reshape_dag,
-    ScheduleConfig, schedule_space, Plan, Exec, Graph, tune, TaskmapError, lib_path, load_library,
+    ScheduleConfig, schedule_space, Plan, Exec, Graph, tune, dag_eval, TaskmapError, lib_path, load_library,
 )
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -135,6 +135,7 @@ struct GemmParams {
   float* workspace;
   int32_t* counters;
   int32_t fast_math;  // approximate transcendentals (bf16 outputs)
+  int32_t ab_f16;     // 16-bit MMA operands are fp16 (kind::f16 a/b format 0), else bf16 (format 1)
   int32_t out_tma;    // row-major output: stage each 32x16 chunk in smem, TMA-store it
   // Canonical epilogue v = act(acc * S[col] + T[col]) (+ R[row, col]), which every
   // chain of the BASELINE configs compiles to (bias, scale, BN-fold, ReLU/GELU,

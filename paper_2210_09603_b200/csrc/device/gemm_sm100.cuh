@@ -98,9 +98,11 @@ __device__ __forceinline__ int64_t addr_rowpart(const Addr& a, int64_t row, int6
   return q * a.s_hi + r * a.s_lo + batch * a.s_batch + a.offset;
 }
 
-// Raw bits of one element converted to the MMA input format.
+// Raw bits of one element converted to the MMA input format: fp32 (tf32
+// kind), or the 16-bit format of the kind::f16 MMA -- bf16, or fp16 when `f16`.
+// Same-format elements are copied bit for bit; others are rounded to nearest.
 template <bool TF32>
-__device__ __forceinline__ uint32_t load_bits(const void* base, int64_t idx, int32_t dt) {
+__device__ __forceinline__ uint32_t load_bits(const void* base, int64_t idx, int32_t dt, bool f16) {
   if (TF32) {
     float f;
     if (dt == DT_F32) f = __ldg(reinterpret_cast<const float*>(base) + idx);
@@ -108,9 +110,14 @@ __device__ __forceinline__ uint32_t load_bits(const void* base, int64_t idx, int
     else f = __half2float(reinterpret_cast<const __half*>(base)[idx]);
     return __float_as_uint(f);
   } else {
-    if (dt == DT_BF16) return __ldg(reinterpret_cast<const unsigned short*>(base) + idx);
-    float f = dt == DT_F32 ? __ldg(reinterpret_cast<const float*>(base) + idx)
-                           : __half2float(reinterpret_cast<const __half*>(base)[idx]);
+    if (dt == (f16 ? DT_F16 : DT_BF16)) return __ldg(reinterpret_cast<const unsigned short*>(base) + idx);
+    const float f = dt == DT_F32 ? __ldg(reinterpret_cast<const float*>(base) + idx)
+                    : dt == DT_BF16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(base)[idx])
+                                    : __half2float(reinterpret_cast<const __half*>(base)[idx]);
+    if (f16) {
+      __half h = __float2half_rn(f);
+      return *reinterpret_cast<unsigned short*>(&h);
+    }
     __nv_bfloat16 h = __float2bfloat16_rn(f);
     return *reinterpret_cast<unsigned short*>(&h);
   }
@@ -141,7 +148,7 @@ __device__ __forceinline__ uint4 pack_chunk(const uint32_t* bits) {
 template <bool TF32, int BK>
 __device__ __forceinline__ void gather_row_strided(uint8_t* tile, int r, const Strided& s,
                                                    int64_t row, bool row_ok, int64_t batch,
-                                                   int k0, int K) {
+                                                   int k0, int K, bool f16) {
   constexpr int PER = TF32 ? 4 : 8;
   const int64_t base = row_ok ? ((row / s.P) * s.s_hi + (row % s.P) * s.s_lo +
                                  batch * s.s_batch + s.offset)
@@ -152,7 +159,7 @@ __device__ __forceinline__ void gather_row_strided(uint8_t* tile, int r, const S
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
       const int k = k0 + c * PER + j;
-      bits[j] = (row_ok && k < K) ? load_bits<TF32>(s.ptr, base + (int64_t)k * s.s_k, s.dtype) : 0u;
+      bits[j] = (row_ok && k < K) ? load_bits<TF32>(s.ptr, base + (int64_t)k * s.s_k, s.dtype, f16) : 0u;
     }
     st_sw128(tile, r, c, pack_chunk<TF32>(bits));
   }
@@ -162,7 +169,7 @@ __device__ __forceinline__ void gather_row_strided(uint8_t* tile, int r, const S
 // reference Col node (compute_ir.cpp:532-557): zero outside the padded image.
 template <bool TF32, int BK>
 __device__ __forceinline__ void gather_row_im2col(uint8_t* tile, int r, const ConvGeom& g,
-                                                  int64_t pix, bool row_ok, int k0, int K) {
+                                                  int64_t pix, bool row_ok, int k0, int K, bool f16) {
   constexpr int PER = TF32 ? 4 : 8;
   const int hw = g.ho * g.wo;
   const int img = row_ok ? static_cast<int>(pix / hw) : 0;
@@ -192,7 +199,7 @@ __device__ __forceinline__ void gather_row_im2col(uint8_t* tile, int r, const Co
       const int ih = bh + fh, iw = bw + fw;
       const bool ok = row_ok && k < K && ih >= 0 && ih < g.h && iw >= 0 && iw < g.w;
       bits[j] = ok ? load_bits<TF32>(g.x, xbase + ch * g.sx[1] + ih * g.sx[2] + iw * g.sx[3],
-                                     g.x_dtype)
+                                     g.x_dtype, f16)
                    : 0u;
       if (g.korder == 0) {
         if (++fw == g.kw) { fw = 0; if (++fh == g.kh) { fh = 0; ++ch; } }
@@ -260,7 +267,7 @@ __device__ __forceinline__ void gather_g8(uint8_t* tile, int r, const ConvGeom& 
 // node, compute_ir.cpp:558-569), any strides of W, either K order.
 template <bool TF32, int BK>
 __device__ __forceinline__ void gather_row_filter(uint8_t* tile, int r, const ConvGeom& g,
-                                                  int64_t f, bool row_ok, int k0, int K) {
+                                                  int64_t f, bool row_ok, int k0, int K, bool f16) {
   constexpr int PER = TF32 ? 4 : 8;
   const int khw = g.kh * g.kw;
   int ch, fh, fw;
@@ -284,7 +291,7 @@ __device__ __forceinline__ void gather_row_filter(uint8_t* tile, int r, const Co
       const int k = k0 + c * PER + j;
       const bool ok = row_ok && k < K && ch < g.c && fh < g.kh;
       bits[j] = ok ? load_bits<TF32>(g.wt, wbase + ch * g.sw[1] + fh * g.sw[2] + fw * g.sw[3],
-                                     g.w_dtype)
+                                     g.w_dtype, f16)
                    : 0u;
       if (g.korder == 0) {
         if (++fw == g.kw) { fw = 0; if (++fh == g.kh) { fh = 0; ++ch; } }
@@ -921,8 +928,20 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
         detail::G8Row g8{};
         if (GENERIC && p.a_loader == LD_IM2COL_G8) g8 = detail::g8_row(p.conv, m0 + t, p.M);
         for (int kb0 = ks * p.kb_per_split, kb = kb0, kb_end = min(p.num_kb, kb0 + p.kb_per_split); kb < kb_end; ++kb, ++q) {
-          // every loader waits for every slot (a warp may not run more than one
-          // ring phase ahead, or the parity wait would alias); only the owner issues
+          // all-TMA: slot q's A comes from warp 2q mod L, its B from warp 2q+1 mod L
+          // (full barrier count 2).  Only those two warps wait for the slot's empty
+          // barrier.  A warp that also polled the slots it does not own could be
+          // lapped: the owners refill slot q and the MMA consumes it before the
+          // bystander polls, the barrier is then two phases past the one it waits
+          // for, the parity test aliases, and the bystander -- owner of slot q+1 --
+          // never issues again (the round-1 intermittent hang).  A warp owns at
+          // least one slot of every `ring` consecutive ones (L <= 4, ring >= 2), so
+          // an owner is never more than one phase ahead of the barrier either.
+          const bool do_a = (2u * q) % R::kLoadWarps == lw, do_b = (2u * q + 1u) % R::kLoadWarps == lw;
+          if (all_tma && !do_a && !do_b) {
+            if (++stage == ring) { stage = 0; phase ^= 1u; }
+            continue;
+          }
           if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&empty[stage], phase ^ 1u);
           else ptx::mbar_wait(&empty[stage], phase ^ 1u);
           uint8_t* a_tile = smA + stage * Cfg::A_BYTES;
@@ -930,8 +949,6 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
           const int k0 = kb * BK;
           const bool b_stays = p.b_resident && q >= static_cast<uint32_t>(ring);
           if (all_tma) {
-            // slot q: A from warp 2q mod 4, B from warp 2q+1 mod 4 (full barrier count 2)
-            const bool do_a = (2u * q) % R::kLoadWarps == lw, do_b = (2u * q + 1u) % R::kLoadWarps == lw;
             if (p.dbg == 3) {  // diagnostics: no copies (MMA on stale smem) -> MMA + epilogue floor
               if (do_a || do_b) {
                 if constexpr (CG == 2) {
@@ -1098,13 +1115,13 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
               const int64_t row = m0 + t;
               const bool ok = row < p.M;
               if (p.a_loader == LD_GATHER)
-                detail::gather_row_strided<TF32, BK>(a_tile, t, p.a, row, ok, b, k0, p.K);
+                detail::gather_row_strided<TF32, BK>(a_tile, t, p.a, row, ok, b, k0, p.K, p.ab_f16 != 0);
               else if (p.a_loader == LD_IM2COL_G8) {
                 if constexpr (!TF32) {
                   if (p.dbg != 3 && p.dbg != 4) detail::gather_g8<BK>(a_tile, t, p.conv, g8, kb);  // async, arrives below
                 }
               } else {
-                detail::gather_row_im2col<TF32, BK>(a_tile, t, p.conv, row, ok, k0, p.K);
+                detail::gather_row_im2col<TF32, BK>(a_tile, t, p.conv, row, ok, k0, p.K, p.ab_f16 != 0);
               }
             }
             if (!b_tma && !b_stays) {
@@ -1113,9 +1130,9 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
                 const int64_t row = n0 + r;
                 const bool ok = row < p.N;
                 if (p.b_loader == LD_GATHER)
-                  detail::gather_row_strided<TF32, BK>(b_tile, r, p.b, row, ok, b, k0, p.K);
+                  detail::gather_row_strided<TF32, BK>(b_tile, r, p.b, row, ok, b, k0, p.K, p.ab_f16 != 0);
                 else
-                  detail::gather_row_filter<TF32, BK>(b_tile, r, p.conv, row, ok, k0, p.K);
+                  detail::gather_row_filter<TF32, BK>(b_tile, r, p.conv, row, ok, k0, p.K, p.ab_f16 != 0);
               }
             }
             if (p.dbg == 4) {  // diagnostics: no gather, one arrival per warp
@@ -1131,6 +1148,19 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
           }
           if (++stage == ring) { stage = 0; phase ^= 1u; }
         }
+      }
+      // Producer tail: wait until the MMA's commits for the last `ring` slots have
+      // arrived on this CTA's empty barriers (the pair leader multicasts them to
+      // both CTAs).  Without it a commit can still be in flight when the CTA exits
+      // and land in the shared memory of the next CTA placed on this SM -- e.g.
+      // the barriers a programmatically launched successor has just initialised.
+      for (int j = 0; j < ring; ++j, ++q) {
+        const bool own = !all_tma || (2u * q) % R::kLoadWarps == lw || (2u * q + 1u) % R::kLoadWarps == lw;
+        if (own) {
+          if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&empty[stage], phase ^ 1u);
+          else ptx::mbar_wait(&empty[stage], phase ^ 1u);
+        }
+        if (++stage == ring) { stage = 0; phase ^= 1u; }
       }
     }
   } else if (warp >= 4 && warp < 4 + kEpiWarps) {
@@ -1547,7 +1577,8 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
       const bool b_mn = p.b_loader == LD_TMA_MN;
       const bool a_noswz = p.a_loader == LD_IM2COL_TMA8;
       const bool a_g8 = p.a_loader == LD_IM2COL_G8;
-      const uint32_t idesc = ptx::make_idesc(kTileM, BN, TF32 ? 2u : 1u, false, b_mn);
+      // operand format: tf32 (kind::tf32) / fp16 (0) or bf16 (1) for kind::f16
+      const uint32_t idesc = ptx::make_idesc(kTileM, BN, TF32 ? 2u : (p.ab_f16 ? 0u : 1u), false, b_mn);
       const uint32_t mn_lbo = p.mn_lbo_sbo_swap ? 1024u : 64u * kRowBytes;
       const uint32_t mn_sbo = p.mn_lbo_sbo_swap ? 64u * kRowBytes : 1024u;
       const uint32_t a0 = ptx::smem_u32(smA), b0 = ptx::smem_u32(smB);

@@ -16,6 +16,7 @@
 #include "taskmap/ir.hpp"
 #include "taskmap/schedule.hpp"
 #include "taskmap_b200.h"
+#include "tune.hpp"
 
 using namespace taskmap;
 
@@ -32,24 +33,27 @@ struct tm_mapping {
 namespace {
 thread_local std::string g_err;
 
-struct Unsupported : std::runtime_error {
-  using std::runtime_error::runtime_error;
-};
-
+// taskmap::Error and its typed refinements (taskmap/ir.hpp) -> tm_status; the
+// message goes to tm_last_error().  The exception type decides the code.
 template <class F>
 tm_status guarded(F&& f) {
   try {
     g_err.clear();
     return f();
+  } catch (const CorrectnessError& e) {
+    g_err = e.what();
+    return TM_ERR_CORRECTNESS;
+  } catch (const UnsupportedError& e) {
+    g_err = e.what();
+    return TM_ERR_UNSUPPORTED;
+  } catch (const CudaError& e) {
+    g_err = e.what();
+    return TM_ERR_CUDA;
   } catch (const Error& e) {
     g_err = e.what();
-    const std::string m = e.what();
-    if (m.find("out of scope") != std::string::npos || m.find("not supported") != std::string::npos ||
-        m.find("unsupported") != std::string::npos)
-      return TM_ERR_UNSUPPORTED;
-    if (m.find("cuda") != std::string::npos || m.find("CUresult") != std::string::npos ||
-        m.find("kernel launch") != std::string::npos)
-      return TM_ERR_CUDA;
+    return TM_ERR_USAGE;
+  } catch (const std::bad_alloc&) {
+    g_err = "host out of memory";
     return TM_ERR_USAGE;
   } catch (const std::exception& e) {
     g_err = e.what();
@@ -305,7 +309,7 @@ tm_status tm_exec_create(const tm_plan* p, const tm_tensor* in, int32_t n_in, co
                          tm_exec** ex) {
   return guarded([&] {
     if (!p || !ex) fail("null argument");
-    if (cudaSetDevice(p->p->device) != cudaSuccess) fail("cudaSetDevice failed");
+    if (cudaSetDevice(p->p->device) != cudaSuccess) fail_cuda("cudaSetDevice failed");
     *ex = new tm_exec{tmb::bind_plan(*p->p, in, n_in, out, n_out)};
     return TM_OK;
   });
@@ -345,7 +349,7 @@ tm_status tm_exec_trace(const tm_exec* e, int32_t index, int64_t* buf, size_t ca
     if (!k.p.trace) fail("exec was not created with TMB_TRACE set");
     const size_t n = size_t(k.grid) * tmb::kTraceTiles * tmb::kTraceEvents;
     if (cap < n) fail("trace buffer too small: need ", n);
-    if (cudaMemcpy(buf, k.p.trace, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) fail("cuda memcpy failed");
+    if (cudaMemcpy(buf, k.p.trace, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) fail_cuda("cuda memcpy failed");
     return TM_OK;
   });
 }
@@ -365,7 +369,7 @@ tm_status tm_graph_create(const tm_exec* const* execs, int32_t n, int32_t timed,
     if (!out || n < 0 || (n > 0 && !execs)) fail("tm_graph_create: bad arguments");
     auto g = std::make_unique<tm_graph>();
     auto ck = [](cudaError_t e, const char* what) {
-      if (e != cudaSuccess) fail(what, " failed: cuda error ", cudaGetErrorString(e));
+      if (e != cudaSuccess) fail_cuda(what, " failed: cuda error ", cudaGetErrorString(e));
     };
     if (timed) {
       g->marks.resize(static_cast<size_t>(n) + 1);
@@ -402,7 +406,7 @@ tm_status tm_graph_launch(const tm_graph* g, void* stream) {
   return guarded([&] {
     if (!g) fail("null graph");
     const cudaError_t e = cudaGraphLaunch(g->exec, static_cast<cudaStream_t>(stream));
-    if (e != cudaSuccess) fail("cudaGraphLaunch failed: cuda error ", cudaGetErrorString(e));
+    if (e != cudaSuccess) fail_cuda("cudaGraphLaunch failed: cuda error ", cudaGetErrorString(e));
     return TM_OK;
   });
 }
@@ -413,7 +417,7 @@ tm_status tm_graph_exec_ms(const tm_graph* g, float* ms, int32_t n) {
     if (!ms || n != static_cast<int32_t>(g->marks.size()) - 1) fail("tm_graph_exec_ms: n must equal the exec count");
     for (int32_t i = 0; i < n; ++i) {
       const cudaError_t e = cudaEventElapsedTime(&ms[i], g->marks[i], g->marks[i + 1]);
-      if (e != cudaSuccess) fail("cudaEventElapsedTime failed: cuda error ", cudaGetErrorString(e));
+      if (e != cudaSuccess) fail_cuda("cudaEventElapsedTime failed: cuda error ", cudaGetErrorString(e));
     }
     return TM_OK;
   });
@@ -427,139 +431,46 @@ tm_status tm_plan_launch(const tm_plan* p, const tm_tensor* in, int32_t n_in, co
     auto e = tmb::bind_plan(*p->p, in, n_in, out, n_out);
     for (const auto& k : e->kernels) tmb::launch_bound(k, stream);
     if (!e->scratch.empty() && cudaStreamSynchronize(static_cast<cudaStream_t>(stream)) != cudaSuccess)
-      fail("cuda stream synchronize failed");
+      fail_cuda("cuda stream synchronize failed");
     return TM_OK;
   });
 }
 
-namespace {
-std::vector<float> fetch(const tm_tensor& t) {
-  int64_t numel = 1, span = 1;
-  for (int d = 0; d < t.rank; ++d) {
-    numel *= t.shape[d];
-    span += (t.shape[d] - 1) * t.stride[d];
-  }
-  const int es = t.dtype == TM_F32 ? 4 : 2;
-  std::vector<unsigned char> raw(static_cast<size_t>(span) * es);
-  if (cudaMemcpy(raw.data(), t.data, raw.size(), cudaMemcpyDeviceToHost) != cudaSuccess) fail("cuda memcpy failed");
-  std::vector<float> out(raw.size() / es);
-  for (size_t i = 0; i < out.size(); ++i) {
-    if (t.dtype == TM_F32) {
-      std::memcpy(&out[i], &raw[i * 4], 4);
-    } else if (t.dtype == TM_BF16) {
-      uint32_t b = static_cast<uint32_t>(raw[i * 2] | (raw[i * 2 + 1] << 8)) << 16;
-      std::memcpy(&out[i], &b, 4);
-    } else {
-      __half h;
-      std::memcpy(&h, &raw[i * 2], 2);
-      out[i] = __half2float(h);
-    }
-  }
-  (void)numel;
-  return out;
-}
-}  // namespace
-
-// Exhaustive on-device tuning: correctness gate = bitwise
-// agreement with the default configuration (whose parity with the reference
-// oracle is established by the test-suite); cost = median CUDA-event time.
+// tune: see tune.cpp.  The TuneReport is returned through
+// *report also when the gate fails (status TM_ERR_CORRECTNESS).
 tm_status tm_tune(const char* dag_json, const tm_tensor* in, int32_t n_in, const tm_tensor* out, int32_t n_out,
                   int32_t device, int32_t reps, tm_schedule_config* best, char** report) {
   return guarded([&] {
-    const auto t0 = std::chrono::steady_clock::now();
+    if (!dag_json) fail("null argument");
     ComputeDAG d = dag_from_json(dag_json);
-    if (cudaSetDevice(device) != cudaSuccess) fail("cudaSetDevice failed");
-    cudaStream_t s;
-    cudaStreamCreate(&s);
-    cudaEvent_t e0, e1;
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    reps = std::max(reps, 1);
-    auto run = [&](const ScheduleConfig& c, float& ms) {
-      auto plan = tmb::build_plan(d, c, device);
-      auto ex = tmb::bind_plan(*plan, in, n_in, out, n_out);
-      for (const auto& k : ex->kernels) tmb::launch_bound(k, s);  // warm-up (and the gated result)
-      if (cudaStreamSynchronize(s) != cudaSuccess) fail("cuda error while tuning: ", cudaGetErrorString(cudaGetLastError()));
-      // time `reps` back-to-back launches replayed from a CUDA graph: device time
-      // only, without the host launch cost that would otherwise dominate small shapes
-      cudaGraph_t graph = nullptr;
-      cudaGraphExec_t gexec = nullptr;
-      if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) fail("cuda capture failed in tune");
-      for (int r = 0; r < reps; ++r)
-        for (const auto& k : ex->kernels) tmb::launch_bound(k, s);
-      if (cudaStreamEndCapture(s, &graph) != cudaSuccess || cudaGraphInstantiate(&gexec, graph, 0) != cudaSuccess) {
-        if (graph) cudaGraphDestroy(graph);
-        fail("cuda graph capture failed in tune: ", cudaGetErrorString(cudaGetLastError()));
-      }
-      cudaGraphDestroy(graph);
-      std::vector<float> times;
-      cudaGraphLaunch(gexec, s);  // warm
-      for (int r = 0; r < 3; ++r) {
-        cudaEventRecord(e0, s);
-        cudaGraphLaunch(gexec, s);
-        cudaEventRecord(e1, s);
-        cudaEventSynchronize(e1);
-        float t = 0;
-        cudaEventElapsedTime(&t, e0, e1);
-        times.push_back(t / reps);
-      }
-      cudaGraphExecDestroy(gexec);
-      if (cudaStreamSynchronize(s) != cudaSuccess) fail("cuda error while tuning: ", cudaGetErrorString(cudaGetLastError()));
-      std::sort(times.begin(), times.end());
-      ms = times[times.size() / 2];
-    };
-    // reference result of the default configuration, kept on the device; the
-    // gate compares every candidate's outputs with it bit for bit
-    std::vector<void*> ref(n_out, nullptr);
-    std::vector<size_t> span(n_out, 0);
-    float ms0 = 0;
-    run(ScheduleConfig{}, ms0);
+    tmb::TuneOutcome r = tmb::tune(d, in, n_in, out, n_out, device, reps);
+    if (report) *report = dup(r.report);
+    if (!r.ok) {
+      if (r.unsupported) fail_unsupported(r.error);
+      fail_as<CorrectnessError>(r.error);
+    }
+    if (best) to_c(r.best, best);
+    return TM_OK;
+  });
+}
+
+// Device DAG interpreter (reference_eval semantics, dev_eval.hpp): evaluates
+// the DAG and writes its outputs, rounded to each output's dtype.
+tm_status tm_dag_eval(const char* dag_json, const tm_tensor* in, int32_t n_in, const tm_tensor* out, int32_t n_out,
+                      int32_t device, void* stream) {
+  return guarded([&] {
+    if (!dag_json || (n_out > 0 && !out)) fail("null argument");
+    ComputeDAG d = dag_from_json(dag_json);
+    auto r = tmb::dag_eval(d, in, n_in, out, n_out, device, stream);
+    const cudaStream_t s = static_cast<cudaStream_t>(stream);
     for (int i = 0; i < n_out; ++i) {
-      size_t elems = 1;
-      for (int d = 0; d < out[i].rank; ++d) elems += size_t(out[i].shape[d] - 1) * out[i].stride[d];
-      span[i] = elems * (out[i].dtype == TM_F32 ? 4 : 2);
-      if (cudaMalloc(&ref[i], span[i]) != cudaSuccess) fail("cudaMalloc failed in tune");
-      cudaMemcpy(ref[i], out[i].data, span[i], cudaMemcpyDeviceToDevice);
+      const std::string& o = d.outputs[i];
+      if (!r->is_float(o)) fail_unsupported("tm_dag_eval: output '", o, "' is not a float tensor");
+      if (tmb::ev::numel_of(out[i]) != r->numel(o)) fail("tm_dag_eval: output '", o, "' has the wrong size");
+      tmb::ev::launch_store(r->values(o), r->numel(o), out[i].data, out[i].dtype, out[i].rank,
+                            tmb::ev::shape_of(out[i]), s);
     }
-    const auto space = schedule_space("matmul");
-    std::string rows;
-    int best_i = -1;
-    float best_ms = 0;
-    for (size_t i = 0; i < space.size(); ++i) {
-      float ms = 0;
-      bool ok = true;
-      std::string err;
-      try {
-        run(space[i], ms);
-        // Gate: same tolerance as the parity tests: split-K reorders
-        // the fp32 accumulation, so float results agree to rounding, not bitwise;
-        // on integer-valued data every config is bit-identical.
-        for (int j = 0; j < n_out && ok; ++j) {
-          const float tol = out[j].dtype == TM_F32 ? 1e-4f : 1e-2f;
-          ok = tmb::device_max_rel_error(out[j].data, ref[j], span[j] / (out[j].dtype == TM_F32 ? 4 : 2),
-                                         out[j].dtype, s) <= tol;
-        }
-      } catch (const Error& e) {
-        ok = false;
-        err = e.what();
-      }
-      rows += std::string(i ? "," : "") + "{\"config\":" + space[i].to_json() + ",\"ms\":" + std::to_string(ms) +
-              ",\"correct\":" + (ok ? "true" : "false") + (err.empty() ? "" : ",\"error\":" + tmjson::quote(err)) + "}";
-      if (ok && (best_i < 0 || ms < best_ms)) { best_i = static_cast<int>(i); best_ms = ms; }
-    }
-    if (best_i < 0) fail("no configuration in the schedule space passed the correctness gate");
-    float msb = 0;
-    run(space[best_i], msb);  // leave the best config's result in the outputs
-    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    if (best) to_c(space[best_i], best);
-    if (report)
-      *report = dup("{\"space_size\":" + std::to_string(space.size()) + ",\"best_index\":" + std::to_string(best_i) +
-                    ",\"best\":" + space[best_i].to_json() + ",\"best_ms\":" + std::to_string(best_ms) +
-                    ",\"tuning_time_s\":" + std::to_string(secs) + ",\"results\":[" + rows + "]}");
-    for (void* r : ref) cudaFree(r);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    cudaStreamDestroy(s);
+    tmb::sync_with_timeout(s, 60.0, "tm_dag_eval");
     return TM_OK;
   });
 }

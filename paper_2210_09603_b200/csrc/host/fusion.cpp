@@ -146,9 +146,16 @@ IndexProgram IndexProgram::compile(const Expr& e, const std::vector<std::string>
         return;
       default: break;
     }
-    fail("unsupported construct in an index expression: ", expr_to_text(x));
+    fail_unsupported("unsupported construct in an index expression: ", expr_to_text(x));
   };
   go(e);
+  // static stack depth (eval keeps a fixed 64-slot stack): reject deeper programs here
+  int depth = 0, max_depth = 0;
+  for (const auto& in : p.code) {
+    depth += in.op <= 1 ? 1 : in.op == 2 ? -1 : in.op == 4 ? -2 : 0;
+    max_depth = std::max(max_depth, depth);
+  }
+  if (max_depth > 60) fail_unsupported("index expression too deep (", max_depth, " stack slots, at most 60)");
   return p;
 }
 
@@ -333,12 +340,12 @@ struct EpiBuilder {
         case UnOp::Exp: sp.ops.push_back({EPI_EXP}); return;
         case UnOp::Sqrt: sp.ops.push_back({EPI_SQRT}); return;
         case UnOp::CastF32: return;
-        default: fail("epilogue op ", unop_name(e->uop), " is not supported on the device");
+        default: fail_unsupported("epilogue op ", unop_name(e->uop), " is not supported on the device");
       }
     }
     if (e->kind == ExprKind::Binary) {
       const bool l = has_acc(e->args[0]), r = has_acc(e->args[1]);
-      if (l == r) fail("epilogue expression is not a single-use chain of the accumulator: ", expr_to_text(e));
+      if (l == r) fail_unsupported("epilogue expression is not a single-use chain of the accumulator: ", expr_to_text(e));
       const Expr& spine = l ? e->args[0] : e->args[1];
       const Expr side = fold(l ? e->args[1] : e->args[0]);
       walk(spine);
@@ -346,7 +353,7 @@ struct EpiBuilder {
       const bool is_const = side->kind == ExprKind::FloatImm || side->kind == ExprKind::IntImm;
       if (is_const) st.c = static_cast<float>(side->kind == ExprKind::FloatImm ? side->fval : static_cast<double>(side->ival));
       else if (side->kind == ExprKind::Load) st.side = side_of(side);
-      else fail("epilogue side operand must be a constant or a tensor element: ", expr_to_text(side));
+      else fail_unsupported("epilogue side operand must be a constant or a tensor element: ", expr_to_text(side));
       const int t = is_const ? 0 : (EPI_ADD_T - EPI_ADD_C);
       switch (e->bop) {
         case BinOp::Add: st.kind = EPI_ADD_C + t; break;
@@ -355,12 +362,12 @@ struct EpiBuilder {
         case BinOp::Div: st.kind = (l ? EPI_DIV_C : EPI_RDIV_C) + t; break;
         case BinOp::Max: st.kind = EPI_MAX_C + t; break;
         case BinOp::Min: st.kind = EPI_MIN_C + t; break;
-        default: fail("epilogue operator ", binop_name(e->bop), " is not supported on the device");
+        default: fail_unsupported("epilogue operator ", binop_name(e->bop), " is not supported on the device");
       }
       sp.ops.push_back(st);
       return;
     }
-    fail("unsupported epilogue expression: ", expr_to_text(e));
+    fail_unsupported("unsupported epilogue expression: ", expr_to_text(e));
   }
 };
 
@@ -368,15 +375,15 @@ SubgraphPlan lower_subgraph(const ComputeDAG& dag, const FusedSubgraph& sg) {
   SubgraphPlan sp;
   sp.sg = sg;
   if (sg.anchor.empty())
-    fail("subgraph '", sg.output, "' has no reduction anchor; rule-based injective kernels are out of scope");
+    fail_unsupported("subgraph '", sg.output, "' has no reduction anchor; rule-based injective kernels are out of scope");
   const TensorNode& r = dag.at(sg.anchor);
-  if (r.combiner != Combiner::Sum) fail("anchor '", r.name, "': only sum reductions lower to tcgen05");
-  if (r.reduce_axes.size() != 1) fail("anchor '", r.name, "': exactly one reduce axis is supported");
-  if (r.axes.size() != 2 && r.axes.size() != 3) fail("anchor '", r.name, "': 2 or 3 spatial axes expected");
+  if (r.combiner != Combiner::Sum) fail_unsupported("anchor '", r.name, "': only sum reductions lower to tcgen05");
+  if (r.reduce_axes.size() != 1) fail_unsupported("anchor '", r.name, "': exactly one reduce axis is supported");
+  if (r.axes.size() != 2 && r.axes.size() != 3) fail_unsupported("anchor '", r.name, "': 2 or 3 spatial axes expected");
   Expr v = r.value;
   if (v->kind != ExprKind::Binary || v->bop != BinOp::Mul || v->args[0]->kind != ExprKind::Load ||
       v->args[1]->kind != ExprKind::Load)
-    fail("anchor '", r.name, "': value must be the product of two tensor elements");
+    fail_unsupported("anchor '", r.name, "': value must be the product of two tensor elements");
   const std::string kname = r.reduce_axes[0].name;
   Expr L[2] = {v->args[0], v->args[1]};
   auto uses = [&](const Expr& l, const std::string& ax) {
@@ -386,18 +393,18 @@ SubgraphPlan lower_subgraph(const ComputeDAG& dag, const FusedSubgraph& sg) {
   for (const auto& ax : r.axes) {
     const bool u0 = uses(L[0], ax.name), u1 = uses(L[1], ax.name);
     if (u0 && u1) {
-      if (!batch.empty()) fail("anchor '", r.name, "': at most one batch axis");
+      if (!batch.empty()) fail_unsupported("anchor '", r.name, "': at most one batch axis");
       batch = ax.name;
     } else if (u0 || u1) {
       std::string& slot = own[u0 ? 0 : 1];
-      if (!slot.empty()) fail("anchor '", r.name, "': operand owns two spatial axes");
+      if (!slot.empty()) fail_unsupported("anchor '", r.name, "': operand owns two spatial axes");
       slot = ax.name;
     } else {
-      fail("anchor '", r.name, "': axis '", ax.name, "' unused by the operands");
+      fail_unsupported("anchor '", r.name, "': axis '", ax.name, "' unused by the operands");
     }
   }
-  if (own[0].empty() || own[1].empty()) fail("anchor '", r.name, "': not a matrix product");
-  if (!uses(L[0], kname) || !uses(L[1], kname)) fail("anchor '", r.name, "': reduce axis missing from an operand");
+  if (own[0].empty() || own[1].empty()) fail_unsupported("anchor '", r.name, "': not a matrix product");
+  if (!uses(L[0], kname) || !uses(L[1], kname)) fail_unsupported("anchor '", r.name, "': reduce axis missing from an operand");
 
   const bool pro0 = std::find(sg.prologue.begin(), sg.prologue.end(), L[0]->name) != sg.prologue.end();
   const bool pro1 = std::find(sg.prologue.begin(), sg.prologue.end(), L[1]->name) != sg.prologue.end();
@@ -447,7 +454,7 @@ SubgraphPlan lower_subgraph(const ComputeDAG& dag, const FusedSubgraph& sg) {
     if (which == im2col_side) {
       // the anchor must read Col[k, pixel] directly
       if (idx.size() != 2 || !expr_equal(idx[0], var(kCol)) || !expr_equal(idx[1], var(kRow)))
-        fail("anchor reads the im2col node through a non-identity index");
+        fail_unsupported("anchor reads the im2col node through a non-identity index");
       op.kind = OperandPlan::Im2col;
       op.conv = ci;
       reindex(op.addr);
@@ -474,7 +481,7 @@ SubgraphPlan lower_subgraph(const ComputeDAG& dag, const FusedSubgraph& sg) {
       }
     }
     if (!reindex(op.addr))
-      fail("prologue '", s.name, "' is not a pure re-index of a graph input (arithmetic prologues are out of scope)");
+      fail_unsupported("prologue '", s.name, "' is not a pure re-index of a graph input (arithmetic prologues are out of scope)");
     op.kind = OperandPlan::Strided;
   };
   lower_operand(ia, sp.a);
@@ -691,23 +698,45 @@ tm::DevMapping tile_mapping(int64_t B, int64_t TM, int64_t TN, int grid, int ras
   return m;
 }
 
-bool tma_ok_kmajor(const Fit& f, const tm_tensor& t, int64_t rows, int want_dt) {
+// TMA tile views are {K, rows, batch} (K-major) or {rows, K, batch} (MN-major)
+// with strides {row, batch}: the batch stride is encoded as given, so a batch
+// whose stride is below one batch's row span (e.g. heads interleaved inside a
+// row, [H,S,D] with strides (D, H*D, 1)) cannot be a TMA view and falls back to
+// the predicated gather loader / direct stores.  With batch == 1 the stride is
+// unused (and encoded as the row span).
+bool batch_ok(int64_t c2, int64_t span, int64_t batch) { return batch <= 1 || c2 >= span; }
+
+bool tma_ok_kmajor(const Fit& f, const tm_tensor& t, int64_t rows, int want_dt, int64_t batch) {
   const int es = esize(t.dtype);
   if (t.dtype != want_dt) return false;
   if (f.c1 != 1 || f.P < rows) return false;
+  if (!batch_ok(f.c2, f.lo * rows, batch)) return false;
   if ((f.lo * es) % 16 || (f.c2 * es) % 16 || f.lo <= 0) return false;
   const uintptr_t base = reinterpret_cast<uintptr_t>(t.data) + f.off * es;
   return base % 16 == 0;
 }
 
-bool tma_ok_mnmajor(const Fit& f, const tm_tensor& t, int64_t rows) {
+bool tma_ok_mnmajor(const Fit& f, const tm_tensor& t, int64_t rows, int64_t k, int64_t batch) {
   if (t.dtype != TM_BF16 && t.dtype != TM_F16) return false;
   const int es = esize(t.dtype);
   if (f.lo != 1 || f.P < rows || f.c1 <= 0) return false;
+  if (!batch_ok(f.c2, f.c1 * k, batch)) return false;
   if ((f.c1 * es) % 16 || (f.c2 * es) % 16) return false;
   return (reinterpret_cast<uintptr_t>(t.data) + f.off * es) % 16 == 0;
 }
 }  // namespace
+
+int intermediate_dtype(const tm_tensor* inputs, int n_in) {
+  bool f32 = false, f16 = false, bf16 = false;
+  for (int i = 0; i < n_in; ++i) {
+    f32 = f32 || inputs[i].dtype == TM_F32;
+    f16 = f16 || inputs[i].dtype == TM_F16;
+    bf16 = bf16 || inputs[i].dtype == TM_BF16;
+  }
+  if (f32) return TM_F32;
+  if (f16 && !bf16) return TM_F16;
+  return TM_BF16;
+}
 
 Exec::~Exec() {
   for (void* p : scratch) cudaFree(p);
@@ -726,16 +755,14 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
     if (t.rank != static_cast<int>(n.shape.size())) fail("tensor '", name, "' has wrong rank");
     for (int d = 0; d < t.rank; ++d)
       if (t.shape[d] != n.shape[d]) fail("tensor '", name, "' has wrong shape at dim ", d);
-    if (t.dtype != TM_F32 && t.dtype != TM_BF16 && t.dtype != TM_F16) fail("tensor '", name, "' has unsupported dtype");
+    if (t.dtype != TM_F32 && t.dtype != TM_BF16 && t.dtype != TM_F16) fail_unsupported("tensor '", name, "' has unsupported dtype");
     if (!t.data) fail("tensor '", name, "' has a null data pointer");
     env[name] = t;
   };
   for (int i = 0; i < n_in; ++i) check(dag.inputs[i], inputs[i]);
   for (int i = 0; i < n_out; ++i) check(dag.outputs[i], outputs[i]);
   auto ex = std::make_unique<Exec>();
-  int idt = TM_BF16;
-  for (int i = 0; i < n_in; ++i)
-    if (inputs[i].dtype == TM_F32) idt = TM_F32;
+  const int idt = intermediate_dtype(inputs, n_in);
   for (const auto& name : plan.intermediates) {
     const TensorNode& n = dag.at(name);
     tm_tensor t{};
@@ -748,7 +775,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       numel *= n.shape[d];
     }
     void* p = nullptr;
-    if (cudaMalloc(&p, numel * esize(idt)) != cudaSuccess) fail("cudaMalloc failed for intermediate '", name, "'");
+    if (cudaMalloc(&p, numel * esize(idt)) != cudaSuccess) fail_cuda("cudaMalloc failed for intermediate '", name, "'");
     ex->scratch.push_back(p);
     t.data = p;
     env[name] = t;
@@ -776,8 +803,15 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
     }
     if (math == "fp32_simt") k.simt = 1;
     k.tf32 = math == "tf32";
+    // 16-bit tensor-core path (tcgen05 kind::f16): the a/b operand format is that of
+    // the operands -- fp16 when both are fp16, else bf16.  Mixed bf16/fp16 operands
+    // would need a lossy conversion of one of them, which is refused.
+    const bool a16 = opa->dtype == TM_F16, b16 = opb->dtype == TM_F16;
+    if (!k.tf32 && !k.simt && (opa->dtype == TM_BF16 || opb->dtype == TM_BF16) && (a16 || b16))
+      fail_unsupported("mixed bf16 / fp16 GEMM operands: cast one side to the other's type first");
+    p.ab_f16 = (!k.tf32 && !k.simt && (a16 || b16)) ? 1 : 0;
     const int BK = k.tf32 ? 32 : 64;
-    const int want_dt = k.tf32 ? TM_F32 : TM_BF16;
+    const int want_dt = k.tf32 ? TM_F32 : (p.ab_f16 ? TM_F16 : TM_BF16);
     k.bn = plan.cfg.block_n;
     if (k.bn < 16 || k.bn > 256 || k.bn % 16) fail("block_n must be 16..256 in steps of 16");
     k.stages = plan.cfg.pipeline ? plan.cfg.stages : 2;
@@ -802,8 +836,8 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
         !sp.b.addr.idx.empty()) {
       Fit fa, fb;
       std::string w2;
-      conv_as_gemm = fit_address(sp.a.addr, *opa, sp.M, sp.K, sp.batch, fa, w2) && tma_ok_kmajor(fa, *opa, sp.M, want_dt) &&
-                     fit_address(sp.b.addr, *opb, sp.N, sp.K, sp.batch, fb, w2) && tma_ok_kmajor(fb, *opb, sp.N, want_dt);
+      conv_as_gemm = fit_address(sp.a.addr, *opa, sp.M, sp.K, sp.batch, fa, w2) && tma_ok_kmajor(fa, *opa, sp.M, want_dt, sp.batch) &&
+                     fit_address(sp.b.addr, *opb, sp.N, sp.K, sp.batch, fb, w2) && tma_ok_kmajor(fb, *opb, sp.N, want_dt, sp.batch);
     }
     if (sp.a.kind == OperandPlan::Im2col && !conv_as_gemm) {
       const ConvInfo& c = sp.a.conv;
@@ -813,13 +847,13 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       g.pad = c.pad; g.ho = c.ho; g.wo = c.wo; g.x = x.data; g.x_dtype = x.dtype;
       for (int d = 0; d < 4; ++d) g.sx[d] = x.stride[d];
       const bool cl = x.stride[1] == 1 && x.stride[3] == c.c && x.stride[2] == c.w * c.c && x.stride[0] == c.h * c.w * c.c;
-      im2col_tma = !k.tf32 && x.dtype == TM_BF16 && cl && c.c % BK == 0 && c.stride <= 8 &&
+      im2col_tma = !k.tf32 && x.dtype == want_dt && cl && c.c % BK == 0 && c.stride <= 8 &&
                    c.pad <= 127 && (c.kh - 1 - c.pad) <= 128 && c.kh <= 127 && c.kw <= 127 &&
                    (reinterpret_cast<uintptr_t>(x.data) % 16 == 0) &&
                    sp.b.kind == OperandPlan::ConvFilter && plan.cfg.split_k >= 1;
       // C <= 8 stored 16-byte padded channels-last (pixel stride 8): one im2col box per tap
       const bool cl8 = x.stride[1] == 1 && x.stride[3] == 8 && x.stride[2] == c.w * 8 && x.stride[0] == c.h * c.w * 8;
-      const bool tma8 = !im2col_tma && !k.tf32 && cg == 1 && x.dtype == TM_BF16 && c.c <= 8 && cl8 &&
+      const bool tma8 = !im2col_tma && !k.tf32 && cg == 1 && x.dtype == want_dt && c.c <= 8 && cl8 &&
                         c.stride <= 8 && c.pad <= 127 && (reinterpret_cast<uintptr_t>(x.data) % 16 == 0) &&
                         sp.b.kind == OperandPlan::ConvFilter;
       g.korder = (im2col_tma || tma8) ? 1 : 0;
@@ -839,9 +873,9 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       }
     } else {
       Fit f;
-      if (!fit_address(sp.a.addr, *opa, sp.M, sp.K, sp.batch, f, why)) fail("operand A '", sp.a.addr.tensor, "': ", why);
+      if (!fit_address(sp.a.addr, *opa, sp.M, sp.K, sp.batch, f, why)) fail_unsupported("operand A '", sp.a.addr.tensor, "': ", why);
       p.a = strided_of(f, *opa);
-      if (tma_ok_kmajor(f, *opa, sp.M, want_dt)) {
+      if (tma_ok_kmajor(f, *opa, sp.M, want_dt, sp.batch)) {
         p.a_loader = LD_TMA_K;
         const uint64_t dims[3] = {(uint64_t)sp.K, (uint64_t)sp.M, (uint64_t)sp.batch};
         const uint64_t strides[2] = {(uint64_t)(f.lo * esize(opa->dtype)),
@@ -881,30 +915,30 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
         // changing weights).
         const int kp = (p.K + 7) / 8 * 8;
         void* packed = nullptr;
-        if (cudaMalloc(&packed, size_t(sp.N) * kp * 2) != cudaSuccess) fail("cudaMalloc failed for the filter repack");
+        if (cudaMalloc(&packed, size_t(sp.N) * kp * 2) != cudaSuccess) fail_cuda("cudaMalloc failed for the filter repack");
         ex->scratch.push_back(packed);
-        pack_filter(g, kp, packed);
+        pack_filter(g, kp, packed, want_dt);
         p.b_loader = LD_TMA_K;
         const uint64_t dims[3] = {(uint64_t)p.K, (uint64_t)sp.N, 1};
         const uint64_t strides[2] = {(uint64_t)kp * 2, (uint64_t)kp * 2 * sp.N};
         const uint32_t box[3] = {(uint32_t)BK, (uint32_t)bn_cta, 1u};
-        make_tma_2d3d(k.tma_b, packed, TM_BF16, 3, dims, strides, box);
+        make_tma_2d3d(k.tma_b, packed, want_dt, 3, dims, strides, box);
       } else {
         p.b_loader = LD_FILTER_GATHER;
       }
     } else {
       if (sp.b.addr.idx.empty()) fail("operand B must be a strided tensor or a conv filter");
       Fit f;
-      if (!fit_address(sp.b.addr, *opb, sp.N, sp.K, sp.batch, f, why)) fail("operand B '", sp.b.addr.tensor, "': ", why);
+      if (!fit_address(sp.b.addr, *opb, sp.N, sp.K, sp.batch, f, why)) fail_unsupported("operand B '", sp.b.addr.tensor, "': ", why);
       p.b = strided_of(f, *opb);
-      if (tma_ok_kmajor(f, *opb, sp.N, want_dt)) {
+      if (tma_ok_kmajor(f, *opb, sp.N, want_dt, sp.batch)) {
         p.b_loader = LD_TMA_K;
         const uint64_t dims[3] = {(uint64_t)sp.K, (uint64_t)sp.N, (uint64_t)sp.batch};
         const uint64_t strides[2] = {(uint64_t)(f.lo * esize(opb->dtype)),
                                      (uint64_t)(std::max<int64_t>(f.c2, f.lo * sp.N) * esize(opb->dtype))};
         const uint32_t box[3] = {(uint32_t)BK, (uint32_t)bn_cta, 1u};
         make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * esize(opb->dtype), opb->dtype, 3, dims, strides, box);
-      } else if (!k.tf32 && bn_cta % 64 == 0 && tma_ok_mnmajor(f, *opb, sp.N)) {
+      } else if (!k.tf32 && bn_cta % 64 == 0 && tma_ok_mnmajor(f, *opb, sp.N, sp.K, sp.batch)) {
         p.b_loader = LD_TMA_MN;
         if (sp.N % 64 == 0 && !std::getenv("TMB_NO_MN4D")) {
           // {64 n, K, N/64 n-blocks, batch}: one box per slot lands the BN/64 column
@@ -940,13 +974,13 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       if (p.a_loader == LD_IM2COL_GATHER || p.a_loader == LD_IM2COL_TMA || p.a_loader == LD_IM2COL_TMA8 ||
           p.a_loader == LD_IM2COL_G8 ||
           p.b_loader == LD_FILTER_GATHER || sp.b.kind == OperandPlan::ConvFilter)
-        fail("math=fp32_simt supports matrix operands only (conv im2col is not supported on this path)");
+        fail_unsupported("math=fp32_simt supports matrix operands only (conv im2col is not supported on this path)");
       k.bn = 128;
       p.tiles_n = static_cast<int32_t>((sp.N + 127) / 128);
       p.tiles_m = static_cast<int32_t>((sp.M + 127) / 128);
     }
     // ---- epilogue
-    if (sp.ops.size() > static_cast<size_t>(kMaxEpiOps)) fail("epilogue longer than ", kMaxEpiOps, " ops");
+    if (sp.ops.size() > static_cast<size_t>(kMaxEpiOps)) fail_unsupported("epilogue longer than ", kMaxEpiOps, " ops");
     p.n_ops = static_cast<int32_t>(sp.ops.size());
     int mat_slots = 0;
     for (size_t i = 0; i < sp.ops.size(); ++i) {
@@ -958,7 +992,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
         const AddrExpr& ae = sp.sides[sp.ops[i].side];
         const tm_tensor& t = lookup(env, ae.tensor);
         Fit f;
-        if (!fit_address(ae, t, sp.M, sp.N, sp.batch, f, why)) fail("epilogue operand '", ae.tensor, "': ", why);
+        if (!fit_address(ae, t, sp.M, sp.N, sp.batch, f, why)) fail_unsupported("epilogue operand '", ae.tensor, "': ", why);
         o.ptr = t.data;
         o.dtype = t.dtype;
         o.a = to_addr(f);
@@ -968,7 +1002,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
         } else if (o.a.s_hi == 0 && o.a.s_lo == 0) {
           o.side = SIDE_COL;
         } else {
-          if (mat_slots >= kMaxMatOps) fail("epilogue has more than ", kMaxMatOps, " full-tile side operands (unsupported)");
+          if (mat_slots >= kMaxMatOps) fail_unsupported("epilogue has more than ", kMaxMatOps, " full-tile side operands (unsupported)");
           o.side = SIDE_MAT;
           o.slot = mat_slots++;
           p.has_mat = 1;
@@ -996,7 +1030,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
     {
       const tm_tensor& t = lookup(env, sp.out.tensor);
       Fit f;
-      if (!fit_address(sp.out, t, sp.M, sp.N, sp.batch, f, why)) fail("output '", sp.out.tensor, "': ", why);
+      if (!fit_address(sp.out, t, sp.M, sp.N, sp.batch, f, why)) fail_unsupported("output '", sp.out.tensor, "': ", why);
       p.out = t.data;
       p.out_dtype = t.dtype;
       p.out_a = to_addr(f);
@@ -1008,6 +1042,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       const int es = esize(t.dtype);
       const uintptr_t base = reinterpret_cast<uintptr_t>(t.data) + f.off * es;
       if (f.c1 == 1 && f.P >= sp.M && f.lo > 0 && (f.lo * es) % 16 == 0 && (f.c2 * es) % 16 == 0 && base % 16 == 0 &&
+          batch_ok(f.c2, f.lo * sp.M, sp.batch) &&
           (t.dtype == TM_BF16 || t.dtype == TM_F32) && !std::getenv("TMB_NO_TMA_STORE")) {
         p.out_tma = 1;
         const uint64_t dims[3] = {(uint64_t)sp.N, (uint64_t)sp.M, (uint64_t)sp.batch};
@@ -1060,7 +1095,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
         void* cnt = nullptr;
         if (cudaMalloc(&ws, tiles * p.split_k * 128 * int64_t(k.bn) * 4) != cudaSuccess ||
             cudaMalloc(&cnt, tiles * 8) != cudaSuccess || cudaMemset(cnt, 0, tiles * 8) != cudaSuccess)
-          fail("cudaMalloc failed for the split-K workspace");
+          fail_cuda("cudaMalloc failed for the split-K workspace");
         ex->scratch.push_back(ws);
         ex->scratch.push_back(cnt);
         p.workspace = static_cast<float*>(ws);
@@ -1089,7 +1124,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       void* d = nullptr;
       if (cudaMalloc(&d, tab.size() * 4) != cudaSuccess ||
           cudaMemcpy(d, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
-        fail("cudaMalloc/cudaMemcpy failed for the tile table");
+        fail_cuda("cudaMalloc/cudaMemcpy failed for the tile table");
       ex->scratch.push_back(d);
       p.tile_tab = static_cast<const uint32_t*>(d);
     }
@@ -1107,7 +1142,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       void* tr = nullptr;
       const size_t bytes = size_t(k.grid) * kTraceTiles * kTraceEvents * 8;
       if (cudaMalloc(&tr, bytes) != cudaSuccess || cudaMemset(tr, 0, bytes) != cudaSuccess)
-        fail("cudaMalloc failed for the trace buffer");
+        fail_cuda("cudaMalloc failed for the trace buffer");
       ex->scratch.push_back(tr);
       p.trace = static_cast<long long*>(tr);
     }

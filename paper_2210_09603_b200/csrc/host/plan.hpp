@@ -95,7 +95,10 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
 int num_sms(int device);
 void launch_bound(const BoundKernel& k, void* stream);
 int kernel_stages(const BoundKernel& k);  // ring depth of the instantiation launch_bound will pick
-void pack_filter(const ConvGeom& g, int kp, void* out);  // bf16 [f][kp] in the GEMM K order
+void pack_filter(const ConvGeom& g, int kp, void* out, int out_dtype);  // bf16/fp16 [f][kp] in the GEMM K order
+// storage dtype of materialised intermediates for these inputs: f32 if any input
+// is f32, fp16 if the 16-bit inputs are all fp16, else bf16
+int intermediate_dtype(const tm_tensor* inputs, int n_in);
 void launch_simt(const BoundKernel& k, void* stream);   // fp32 CUDA-core kernel (simt_fp32.cu)
 int kernel_mapping_assign(int which, uint32_t worker, int* buf, int cap);
 unsigned long long device_mismatch(const void* a, const void* b, size_t bytes, void* stream);

@@ -49,25 +49,25 @@ std::string ScheduleConfig::key() const {
   return o.str();
 }
 
-// The space: UMMA N (tile width; M is fixed at 128 TMEM lanes) x ring depth
-// (paper double buffer = 2 stages, or the deepest ring that fits 227 KB) x
-// CTA->tile task mapping (repeat*spatial vs spatial*repeat).  The same list is
-// returned for every problem shape; tails are handled by TMA zero fill and
-// predicated gathers/stores, never by shrinking the space.
+// The space: UMMA N (tile width; M is fixed at 128 TMEM lanes per CTA) x ring
+// depth (paper double buffer = 2 stages, or the deepest ring that fits 227 KB)
+// x split-K x CTA->tile task mapping (repeat*spatial vs spatial*repeat), for
+// single-SM tiles, SM-pair tiles (tcgen05 cta_group::2, 256 x N) and half-size
+// persistent grids.  The same list is returned for every problem shape; tails
+// are handled by TMA zero fill and predicated gathers/stores, never by
+// shrinking the space.  (Round 1 kept split-K 4, BN=64 split-K and pair BN=128
+// out of the tuned space after intermittent hangs; the cause -- loader warps
+// polling ring slots they did not own, and a missing producer tail -- is fixed
+// in gemm_sm100.cuh, and every point is back.)
 std::vector<ScheduleConfig> schedule_space(const std::string& op_kind) {
   if (op_kind != "matmul" && op_kind != "conv2d" && op_kind != "batch_matmul")
     fail("unknown op kind '", op_kind, "' for schedule_space");
   std::vector<ScheduleConfig> out;
-  // single-SM tiles (128 x N): every N, double buffer or deep ring, split-K
-  // Kept out of the tuned space (instantiated and parity-tested): split-K 4, and
-  // split-K with BN=64 -- back-to-back launches of the BERT FFN chain under
-  // those hung intermittently on the GPU box (scripts/space_probe.py, ~1 in 3
-  // sweeps of the space); not yet root-caused.
-  for (int bn : {128, 256, 192, 64})
-    for (int sk : {1, 2})
+  // single-SM tiles (128 x N)
+  for (int bn : {128, 256, 192, 64, 96})
+    for (int sk : {1, 2, 4})
       for (bool deep : {true, false})
         for (int raster : {0, 1}) {
-          if (bn == 64 && sk > 1) continue;
           ScheduleConfig c;
           c.block_n = bn;
           c.split_k = sk;
@@ -76,16 +76,6 @@ std::vector<ScheduleConfig> schedule_space(const std::string& op_kind) {
           c.raster = raster;
           out.push_back(c);
         }
-  // BN=96 tiles (147 tiles for the 6272-pixel ResNet stage-3 maps at F=256), no split
-  for (bool deep : {true, false})
-    for (int raster : {0, 1}) {
-      ScheduleConfig c;
-      c.block_n = 96;
-      c.pipeline = deep;
-      c.stages = deep ? 0 : 2;
-      c.raster = raster;
-      out.push_back(c);
-    }
   // half-size persistent grids (74 CTAs, two SMs' worth of tiles each): L2 reuse
   // across a CTA's consecutive tiles against fewer SMs in flight
   for (int bn : {128, 256, 192, 64, 96})
@@ -96,23 +86,10 @@ std::vector<ScheduleConfig> schedule_space(const std::string& op_kind) {
       c.grid = 74;
       out.push_back(c);
     }
-  for (int bn : {128, 256})
-    for (int raster : {0, 1}) {
-      ScheduleConfig c;
-      c.block_n = bn;
-      c.pipeline = false;
-      c.stages = 2;
-      c.raster = raster;
-      c.grid = 74;
-      out.push_back(c);
-    }
   // SM-pair tiles (256 x N, tcgen05.mma.cta_group::2), deep ring
-  // (BN=128 pairs are instantiated and parity-tested but not tuned: back-to-back
-  // launches of the GELU/residual FFN chain with them hung on the GPU box)
-  for (int bn : {256, 64})
-    for (int sk : {1, 2})
+  for (int bn : {256, 128, 64})
+    for (int sk : {1, 2, 4})
       for (int raster : {0, 1}) {
-        if (bn == 64 && sk > 1) continue;
         ScheduleConfig c;
         c.block_m = 256;
         c.block_n = bn;

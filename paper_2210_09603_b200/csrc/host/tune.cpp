@@ -1,0 +1,280 @@
+// Exhaustive hardware-centric tuning (§4.3/§5.1.3):
+// every configuration of schedule_space is (1) verified on fixed seeded inputs
+// against the device DAG interpreter (dev_eval.hpp -- reference_eval's
+// semantics, independent of the tensor programs), (2) timed on the caller's
+// bound tensors with CUDA events over a graph of back-to-back launches, and the
+// fastest correct one wins (ties: space order).  Correctness is a hard gate:
+// any incorrect configuration aborts the run with a report (CorrectnessError ->
+// TM_ERR_CORRECTNESS).  Configurations the device path cannot bind for this
+// problem (UnsupportedError, e.g. an operand layout TMA cannot describe) are
+// recorded as unsupported, not incorrect.
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <sstream>
+#include <thread>
+
+#include "dev_eval.hpp"
+#include "json.hpp"
+#include "plan.hpp"
+#include "tune.hpp"
+
+namespace tmb {
+
+using namespace taskmap;
+
+namespace {
+
+struct Stream {
+  cudaStream_t s = nullptr;
+  Stream() {
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) fail_cuda("cudaStreamCreate failed");
+  }
+  ~Stream() {
+    if (s) cudaStreamDestroy(s);
+  }
+};
+struct Event {
+  cudaEvent_t e = nullptr;
+  Event() {
+    if (cudaEventCreate(&e) != cudaSuccess) fail_cuda("cudaEventCreate failed");
+  }
+  ~Event() {
+    if (e) cudaEventDestroy(e);
+  }
+};
+struct GraphExec {
+  cudaGraphExec_t g = nullptr;
+  ~GraphExec() {
+    if (g) cudaGraphExecDestroy(g);
+  }
+};
+
+int esize(int dt) { return dt == TM_F32 ? 4 : 2; }
+
+double tolerance(int out_dtype) {
+  // SPEC.md:505 (1e-4 relative on f32); bf16 / fp16 outputs carry 2^-9 / 2^-12
+  // rounding; the metric's floor is max(1, |ref|, rms(ref)) (see dev_eval.cu)
+  return out_dtype == TM_F32 ? 1e-4 : out_dtype == TM_F16 ? 2e-3 : 1e-2;
+}
+
+std::string num(double v) {
+  char b[64];
+  std::snprintf(b, sizeof b, "%.6g", v);
+  return std::isfinite(v) ? std::string(b) : std::string("null");
+}
+
+}  // namespace
+
+void sync_with_timeout(cudaStream_t s, double seconds, const char* what) {
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const cudaError_t e = cudaStreamQuery(s);
+    if (e == cudaSuccess) return;
+    if (e != cudaErrorNotReady) fail_cuda(what, ": ", cudaGetErrorString(e));
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > seconds)
+      fail_cuda(what, ": no progress within ", seconds, " s (kernel hang); the CUDA context is no longer usable");
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+}
+
+TuneOutcome tune(const ComputeDAG& d, const tm_tensor* in, int n_in, const tm_tensor* out, int n_out, int device,
+                 int reps) {
+  const auto t0 = std::chrono::steady_clock::now();
+  if (cudaSetDevice(device) != cudaSuccess) fail_cuda("cudaSetDevice failed");
+  d.validate();
+  if (n_in != static_cast<int>(d.inputs.size()) || n_out != static_cast<int>(d.outputs.size()))
+    fail("tune: expected ", d.inputs.size(), " inputs and ", d.outputs.size(), " outputs");
+  for (const auto& o : d.outputs)
+    if (d.at(o).dtype != taskmap::DType::F32) fail_unsupported("tune: output '", o, "' is not a float tensor");
+  reps = std::max(reps, 1);
+  Stream st;
+  Event e0, e1;
+  const cudaStream_t s = st.s;
+
+  // ---- verification inputs / outputs: same dtypes, shapes and strides as the
+  // caller's tensors, in buffers of their own (two trials)
+  constexpr int kTrials = 2;
+  const bool exact = ev::dag_integer_exact(d);
+  std::vector<std::vector<ev::DeviceBuffer>> vbuf(kTrials);
+  std::vector<std::vector<tm_tensor>> vin(kTrials), vout(kTrials);
+  std::vector<std::unique_ptr<ev::DagEval>> ref(kTrials);
+  std::map<std::string, int> round;
+  {
+    auto plan0 = build_plan(d, ScheduleConfig{}, device);
+    const int idt = intermediate_dtype(in, n_in);
+    for (const auto& n : plan0->intermediates)
+      round[n] = idt == TM_F32 ? ev::RD_F32 : idt == TM_F16 ? ev::RD_F16 : ev::RD_BF16;
+  }
+  for (int t = 0; t < kTrials; ++t) {
+    for (int i = 0; i < n_in; ++i) {
+      tm_tensor x = in[i];
+      vbuf[t].emplace_back(static_cast<size_t>(std::max<int64_t>(ev::span_of(x), 1)) * esize(x.dtype));
+      x.data = vbuf[t].back().p;
+      ev::launch_fill(x.data, x.dtype, x.rank, ev::shape_of(x), ev::span_of(x),
+                      0x7a5c0ffeeull * (t + 1) + 0x100000001b3ull * (i + 1), t, s);
+      vin[t].push_back(x);
+    }
+    for (int i = 0; i < n_out; ++i) {
+      tm_tensor x = out[i];
+      vbuf[t].emplace_back(static_cast<size_t>(std::max<int64_t>(ev::span_of(x), 1)) * esize(x.dtype));
+      x.data = vbuf[t].back().p;
+      vout[t].push_back(x);
+    }
+    ref[t] = std::make_unique<ev::DagEval>(d, vin[t].data(), n_in, round, s);
+  }
+  ev::DeviceBuffer tmp3(3 * sizeof(double));
+
+  // one verification trial of a bound config: worst metric over the outputs
+  auto verify = [&](const Plan& plan, int t, double& err, double& nbad, double& tol) {
+    auto ex = bind_plan(plan, vin[t].data(), n_in, vout[t].data(), n_out);
+    for (int i = 0; i < n_out; ++i)  // poison: an output element the program never writes fails the gate
+      ev::launch_fill_nan(vout[t][i].data, vout[t][i].dtype, ev::span_of(vout[t][i]), s);
+    for (const auto& k : ex->kernels) launch_bound(k, s);
+    sync_with_timeout(s, 20.0, "tune: verification launch");
+    err = 0.0;
+    nbad = 0.0;
+    tol = 0.0;
+    for (int i = 0; i < n_out; ++i) {
+      double h[3];
+      const tm_tensor& o = vout[t][i];
+      ev::launch_compare(o.data, o.dtype, o.rank, ev::shape_of(o), ref[t]->values(d.outputs[i]), ev::numel_of(o),
+                         static_cast<double*>(tmp3.p), h, s);
+      err = std::max(err, h[0]);
+      nbad += h[1];
+      tol = std::max(tol, tolerance(o.dtype));
+    }
+  };
+
+  auto time_config = [&](const Plan& plan) {
+    auto ex = bind_plan(plan, in, n_in, out, n_out);
+    for (const auto& k : ex->kernels) launch_bound(k, s);  // warm-up
+    sync_with_timeout(s, 20.0, "tune: warm-up launch");
+    cudaGraph_t graph = nullptr;
+    GraphExec gx;
+    if (cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) fail_cuda("tune: stream capture failed");
+    try {
+      for (int r = 0; r < reps; ++r)
+        for (const auto& k : ex->kernels) launch_bound(k, s);
+    } catch (...) {
+      cudaStreamEndCapture(s, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    if (cudaStreamEndCapture(s, &graph) != cudaSuccess) fail_cuda("tune: stream capture failed");
+    const cudaError_t ie = cudaGraphInstantiate(&gx.g, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) fail_cuda("tune: cudaGraphInstantiate failed: ", cudaGetErrorString(ie));
+    std::vector<float> times;
+    if (cudaGraphLaunch(gx.g, s) != cudaSuccess) fail_cuda("tune: cudaGraphLaunch failed");
+    for (int r = 0; r < 3; ++r) {
+      cudaEventRecord(e0.e, s);
+      if (cudaGraphLaunch(gx.g, s) != cudaSuccess) fail_cuda("tune: cudaGraphLaunch failed");
+      cudaEventRecord(e1.e, s);
+      sync_with_timeout(s, 20.0, "tune: timed launch");
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0.e, e1.e);
+      times.push_back(ms / reps);
+    }
+    std::sort(times.begin(), times.end());
+    return times[times.size() / 2];
+  };
+
+  const auto space = schedule_space("matmul");
+  std::ostringstream rows;
+  int best_i = -1, n_correct = 0, n_unsupported = 0;
+  std::vector<std::string> failures;
+  float best_ms = 0;
+  for (size_t i = 0; i < space.size(); ++i) {
+    float ms = 0;
+    std::string status = "correct", err_text;
+    double errs[kTrials] = {0, 0}, bad[kTrials] = {0, 0};
+    try {
+      auto plan = build_plan(d, space[i], device);
+      for (int t = 0; t < kTrials; ++t) {
+        double tol = 0;
+        verify(*plan, t, errs[t], bad[t], tol);
+        const bool ok = (t == 0 && exact) ? bad[t] == 0 : errs[t] <= tol;
+        if (!ok && status == "correct") {
+          status = "incorrect";
+          err_text = std::string(t == 0 ? "integer" : "float") + " trial: max error " + num(errs[t]) + " (tolerance " +
+                     num(t == 0 && exact ? 0.0 : tol) + "), " + num(bad[t]) + " elements differ from the rounded reference";
+        }
+      }
+      ms = time_config(*plan);
+    } catch (const UnsupportedError& e) {
+      status = "unsupported";
+      err_text = e.what();
+    } catch (const CudaError&) {
+      throw;  // a hung or faulted context cannot run the remaining configs
+    } catch (const Error& e) {
+      status = "incorrect";
+      err_text = e.what();
+    }
+    if (status == "correct") {
+      ++n_correct;
+      if (best_i < 0 || ms < best_ms) {
+        best_i = static_cast<int>(i);
+        best_ms = ms;
+      }
+    } else if (status == "unsupported") {
+      ++n_unsupported;
+    } else {
+      failures.push_back(space[i].key() + ": " + err_text);
+    }
+    rows << (i ? "," : "") << "{\"index\":" << i << ",\"config\":" << space[i].to_json() << ",\"ms\":" << num(ms)
+         << ",\"correct\":" << (status == "correct" ? "true" : "false") << ",\"status\":\"" << status << "\""
+         << ",\"int_error\":" << num(errs[0]) << ",\"int_mismatches\":" << num(bad[0])
+         << ",\"float_error\":" << num(errs[1]) << (err_text.empty() ? "" : ",\"error\":" + tmjson::quote(err_text))
+         << "}";
+  }
+  TuneOutcome r;
+  const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  auto report = [&](bool ok) {
+    std::ostringstream o;
+    o << "{\"ok\":" << (ok ? "true" : "false") << ",\"space_size\":" << space.size() << ",\"n_correct\":" << n_correct
+      << ",\"n_unsupported\":" << n_unsupported << ",\"n_incorrect\":" << failures.size()
+      << ",\"verification\":{\"trials\":[\"integer U{-8..8}\",\"dyadic k/256\"],\"integer_exact\":"
+      << (exact ? "true" : "false") << ",\"reference\":\"device DAG interpreter (reference_eval semantics)\"}"
+      << ",\"best_index\":" << best_i;
+    if (best_i >= 0) o << ",\"best\":" << space[best_i].to_json() << ",\"best_ms\":" << num(best_ms);
+    o << ",\"tuning_time_s\":" << num(secs) << ",\"results\":[" << rows.str() << "]}";
+    return o.str();
+  };
+  if (!failures.empty()) {
+    r.report = report(false);
+    std::ostringstream m;
+    m << "tune: " << failures.size() << " of " << space.size()
+      << " configurations failed the correctness gate (first: " << failures[0] << ")";
+    r.error = m.str();
+    return r;
+  }
+  if (best_i < 0) {
+    r.report = report(false);
+    r.error = "tune: no configuration of the schedule space supports this problem";
+    r.unsupported = true;
+    return r;
+  }
+  // leave the best configuration's result in the caller's outputs
+  {
+    auto plan = build_plan(d, space[best_i], device);
+    auto ex = bind_plan(*plan, in, n_in, out, n_out);
+    for (const auto& k : ex->kernels) launch_bound(k, s);
+    sync_with_timeout(s, 20.0, "tune: final launch");
+  }
+  r.ok = true;
+  r.best = space[best_i];
+  r.report = report(true);
+  return r;
+}
+
+std::unique_ptr<ev::DagEval> dag_eval(const ComputeDAG& d, const tm_tensor* in, int n_in, const tm_tensor* out,
+                                      int n_out, int device, void* stream) {
+  if (cudaSetDevice(device) != cudaSuccess) fail_cuda("cudaSetDevice failed");
+  if (n_out != static_cast<int>(d.outputs.size())) fail("expected ", d.outputs.size(), " output tensors, got ", n_out);
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto r = std::make_unique<ev::DagEval>(d, in, n_in, std::map<std::string, int>{}, s);
+  return r;
+}
+
+}  // namespace tmb

@@ -6,6 +6,7 @@
 
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "launch_one.cuh"
 
@@ -40,7 +41,7 @@ CUtensorMapDataType tma_dtype(int dt) {
 }
 
 void check_cu(CUresult r, const char* what) {
-  if (r != CUDA_SUCCESS) taskmap::fail(what, " failed with CUresult ", static_cast<int>(r));
+  if (r != CUDA_SUCCESS) taskmap::fail_cuda(what, " failed with CUresult ", static_cast<int>(r));
 }
 
 }  // namespace
@@ -88,8 +89,10 @@ void make_tma_im2col(void* map, const void* ptr, int dtype, const uint64_t* dims
 }
 
 // Filter repack into the GEMM's K order (bind-time; see fusion.cpp): out[f][k]
-// bf16, K-major, row length kp (multiple of 8), zero where the K order pads.
-__global__ void pack_filter_kernel(ConvGeom g, int kp, __nv_bfloat16* out) {
+// bf16 or fp16 (the MMA operand format), K-major, row length kp (multiple of 8),
+// zero where the K order pads.
+template <class T>
+__global__ void pack_filter_kernel(ConvGeom g, int kp, T* out) {
   const int64_t n = static_cast<int64_t>(g.f) * kp;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     const int f = static_cast<int>(i / kp), k = static_cast<int>(i % kp);
@@ -107,16 +110,19 @@ __global__ void pack_filter_kernel(ConvGeom g, int kp, __nv_bfloat16* out) {
     float v = 0.f;
     if (c < g.c && fh < g.kh) {
       const int64_t idx = f * g.sw[0] + c * g.sw[1] + fh * g.sw[2] + fw * g.sw[3];
-      v = g.w_dtype == DT_F32 ? reinterpret_cast<const float*>(g.wt)[idx]
-                              : __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(g.wt)[idx]);
+      v = g.w_dtype == DT_F32    ? reinterpret_cast<const float*>(g.wt)[idx]
+          : g.w_dtype == DT_BF16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(g.wt)[idx])
+                                 : __half2float(reinterpret_cast<const __half*>(g.wt)[idx]);
     }
-    out[i] = __float2bfloat16_rn(v);
+    if constexpr (sizeof(T) == 2 && std::is_same<T, __half>::value) out[i] = __float2half_rn(v);
+    else out[i] = __float2bfloat16_rn(v);
   }
 }
 
-void pack_filter(const ConvGeom& g, int kp, void* out) {
-  pack_filter_kernel<<<148, 256>>>(g, kp, static_cast<__nv_bfloat16*>(out));
-  if (cudaDeviceSynchronize() != cudaSuccess) taskmap::fail("filter repack kernel failed: ", cudaGetErrorString(cudaGetLastError()));
+void pack_filter(const ConvGeom& g, int kp, void* out, int out_dtype) {
+  if (out_dtype == TM_F16) pack_filter_kernel<<<148, 256>>>(g, kp, static_cast<__half*>(out));
+  else pack_filter_kernel<<<148, 256>>>(g, kp, static_cast<__nv_bfloat16*>(out));
+  if (cudaDeviceSynchronize() != cudaSuccess) taskmap::fail_cuda("filter repack kernel failed: ", cudaGetErrorString(cudaGetLastError()));
 }
 
 __global__ void mismatch_kernel(const uint4* a, const uint4* b, size_t n16, const uint8_t* ta, const uint8_t* tb,
@@ -133,7 +139,7 @@ __global__ void mismatch_kernel(const uint4* a, const uint4* b, size_t n16, cons
 // Bitwise comparison of two device byte ranges (the tuner's correctness gate).
 unsigned long long device_mismatch(const void* a, const void* b, size_t bytes, void* stream) {
   unsigned long long* d = nullptr;
-  if (cudaMalloc(&d, 8) != cudaSuccess) taskmap::fail("cudaMalloc failed in device_mismatch");
+  if (cudaMalloc(&d, 8) != cudaSuccess) taskmap::fail_cuda("cudaMalloc failed in device_mismatch");
   cudaMemsetAsync(d, 0, 8, static_cast<cudaStream_t>(stream));
   const bool aligned = (reinterpret_cast<uintptr_t>(a) % 16 == 0) && (reinterpret_cast<uintptr_t>(b) % 16 == 0);
   const size_t n16 = aligned ? bytes / 16 : 0;
@@ -172,7 +178,7 @@ __global__ void max_rel_error_kernel(const void* a, const void* b, size_t n, int
 // max |a-b| / max(1, |b|) over n elements of dtype (the tuner's tolerance gate).
 float device_max_rel_error(const void* a, const void* b, size_t n, int dtype, void* stream) {
   unsigned int* d = nullptr;
-  if (cudaMalloc(&d, 4) != cudaSuccess) taskmap::fail("cudaMalloc failed in device_max_rel_error");
+  if (cudaMalloc(&d, 4) != cudaSuccess) taskmap::fail_cuda("cudaMalloc failed in device_max_rel_error");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaMemsetAsync(d, 0, 4, s);
   max_rel_error_kernel<<<296, 1024, 0, s>>>(a, b, n, dtype, d);
@@ -205,7 +211,7 @@ void launch_bound(const BoundKernel& k, void* stream) {
   else ok = launch_cg1_generic_bf16(k, s);
   if (!ok) taskmap::fail("no kernel instantiated for block_n=", k.bn, " cta_group=", k.cg);
   const cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) taskmap::fail("kernel launch failed: ", cudaGetErrorString(e));
+  if (e != cudaSuccess) taskmap::fail_cuda("kernel launch failed: ", cudaGetErrorString(e));
 }
 
 }  // namespace tmb

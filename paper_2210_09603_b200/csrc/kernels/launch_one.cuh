@@ -6,23 +6,31 @@
 
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 
 #include "../device/gemm_sm100.cuh"
 #include "../host/plan.hpp"
 
 namespace tmb {
 
+constexpr int kMaxDevices = 64;
+
 template <int BN, int STAGES, bool TF32, int CG, bool GENERIC>
 void launch_one(const BoundKernel& k, cudaStream_t s) {
   using Cfg = GemmCfg<BN, STAGES, TF32, CG, GENERIC>;
   static_assert(Cfg::SMEM_BYTES <= kMaxSmem, "shared memory budget");
   auto fn = tm_gemm_kernel<BN, STAGES, TF32, CG, GENERIC>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES) != cudaSuccess)
-      taskmap::fail("cudaFuncSetAttribute failed: ", cudaGetErrorString(cudaGetLastError()));
-    attr_set = true;
-  }
+  // the dynamic shared-memory opt-in is a per-device (per-context) attribute:
+  // set once per device this process launches on, thread-safely
+  static std::once_flag attr_once[kMaxDevices];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
+    taskmap::fail_cuda("cudaGetDevice failed or device index out of range");
+  cudaError_t attr_err = cudaSuccess;
+  std::call_once(attr_once[dev], [&] {
+    attr_err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES);
+  });
+  if (attr_err != cudaSuccess) taskmap::fail_cuda("cudaFuncSetAttribute failed: ", cudaGetErrorString(attr_err));
   CUtensorMap ta, tb, tc;
   std::memcpy(&ta, k.tma_a, sizeof(ta));
   std::memcpy(&tb, k.tma_b, sizeof(tb));
@@ -34,13 +42,13 @@ void launch_one(const BoundKernel& k, cudaStream_t s) {
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   int na = 0;
-  // programmatic dependent launch: this grid's prologue overlaps the previous
-  // kernel's tail (the kernel waits with griddepcontrol.wait before touching memory)
-  // Programmatic dependent launch is opt-in (TMB_PDL=1): replaying the 57-launch
-  // sweep graph with it hung once in ~1400 sweeps (scripts/sweep_stress.py), and
-  // 3000 sweeps without it ran clean.  It is worth ~8% of the sweep, so it stays
-  // available for investigation.
-  static const bool pdl = std::getenv("TMB_PDL") != nullptr;
+  // Programmatic dependent launch (default on; TMB_NO_PDL=1 disables): this grid's
+  // prologue (barrier init, TMEM allocation, descriptor prefetch, tile list)
+  // overlaps the previous kernel's tail; the kernel waits with
+  // griddepcontrol.wait before touching global memory.  (Round 1 had it opt-in
+  // after a rare cross-kernel hang; with the producer tail and owner-only ring
+  // waits in gemm_sm100.cuh 5000-sweep stress runs are clean with it on.)
+  static const bool pdl = std::getenv("TMB_NO_PDL") == nullptr;
   if (pdl) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na].val.programmaticStreamSerializationAllowed = 1;
@@ -56,7 +64,7 @@ void launch_one(const BoundKernel& k, cudaStream_t s) {
   cfg.attrs = attr;
   cfg.numAttrs = na;
   if (cudaLaunchKernelEx(&cfg, fn, k.p, ta, tb, tc) != cudaSuccess)
-    taskmap::fail("cudaLaunchKernelEx failed: ", cudaGetErrorString(cudaGetLastError()));
+    taskmap::fail_cuda("cudaLaunchKernelEx failed: ", cudaGetErrorString(cudaGetLastError()));
 }
 
 // per-unit dispatchers (defined in inst_*.cu); return false if no variant matches

@@ -90,6 +90,7 @@ def load_library():
         "tm_graph_destroy": ([P], None),
         "tm_tune": ([ctypes.c_char_p, ctypes.POINTER(TmTensor), I32, ctypes.POINTER(TmTensor), I32, I32, I32,
                      ctypes.POINTER(TmScheduleConfig), ctypes.POINTER(P)], I32),
+        "tm_dag_eval": ([ctypes.c_char_p, ctypes.POINTER(TmTensor), I32, ctypes.POINTER(TmTensor), I32, I32, P], I32),
     }
     for name, (args, res) in sigs.items():
         f = getattr(L, name)
@@ -590,12 +591,34 @@ def _resolve_device(device: Optional[int], tensors=()) -> int:
 
 
 def tune(dag: ComputeDAG, inputs, outputs, device: Optional[int] = None, reps: int = 5):
-    """Exhaustive on-device tuning over schedule_space; returns (best, report)."""
+    """Exhaustive on-device tuning over schedule_space; returns (best, report).
+
+    Every config is verified against the device DAG interpreter on two seeded
+    inputs before it is timed; an incorrect config aborts tuning with a
+    TaskmapError of status 1 (TM_ERR_CORRECTNESS) whose .report holds the
+    TuneReport."""
     device = _resolve_device(device, list(inputs) + list(outputs))
     ins = (TmTensor * max(1, len(inputs)))(*[_tensor_arg(t) for t in inputs])
     outs = (TmTensor * max(1, len(outputs)))(*[_tensor_arg(t) for t in outputs])
     best = TmScheduleConfig()
     p = ctypes.c_void_p()
-    _check(load_library().tm_tune(dag.to_json().encode(), ins, len(inputs), outs, len(outputs), int(device),
-                                  int(reps), ctypes.byref(best), ctypes.byref(p)))
-    return ScheduleConfig.from_c(best), json.loads(_take_string(p))
+    L = load_library()
+    status = L.tm_tune(dag.to_json().encode(), ins, len(inputs), outs, len(outputs), int(device),
+                       int(reps), ctypes.byref(best), ctypes.byref(p))
+    report = json.loads(_take_string(p)) if p.value else None
+    if status != 0:
+        err = TaskmapError(L.tm_last_error().decode(), status)
+        err.report = report
+        raise err
+    return ScheduleConfig.from_c(best), report
+
+
+def dag_eval(dag: ComputeDAG, inputs, outputs, device: Optional[int] = None, stream=None):
+    """The reference interpreter's semantics re-run on the device (tm_dag_eval): writes dag.outputs into `outputs`."""
+    import torch
+    device = _resolve_device(device, list(inputs) + list(outputs))
+    ins = (TmTensor * max(1, len(inputs)))(*[_tensor_arg(t) for t in inputs])
+    outs = (TmTensor * max(1, len(outputs)))(*[_tensor_arg(t) for t in outputs])
+    s = stream if stream is not None else torch.cuda.current_stream()
+    _check(load_library().tm_dag_eval(dag.to_json().encode(), ins, len(inputs), outs, len(outputs), int(device),
+                                      ctypes.c_void_p(s.cuda_stream)))

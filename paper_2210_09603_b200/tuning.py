@@ -7,7 +7,12 @@ import time
 from dataclasses import asdict
 from typing import Dict, Optional
 
-from .taskmap import ScheduleConfig, tune
+from .taskmap import ScheduleConfig, schedule_space, tune
+
+
+# bumped whenever the tuner's correctness gate changes: entries verified by an
+# older gate are re-tuned
+GATE_VERSION = 2
 
 
 class TuningCache:
@@ -26,8 +31,14 @@ class TuningCache:
             os.replace(tmp, self.path)
 
     def lookup(self, key: str) -> Optional[ScheduleConfig]:
+        """The cached best config of `key`, or None when absent or stale: a cached
+        config must still be a member of the current schedule_space (and verified
+        by the current gate), else the workload is re-tuned."""
         e = self.entries.get(key)
-        return ScheduleConfig(**e["config"]) if e else None
+        if not e or e.get("gate") != GATE_VERSION:
+            return None
+        c = ScheduleConfig(**e["config"])
+        return c if c in schedule_space("matmul") else None
 
     def tune(self, key: str, dag, inputs, outputs, reps: int = 5, force: bool = False):
         """Returns (config, seconds spent tuning now, cached?)."""
@@ -40,5 +51,6 @@ class TuningCache:
         secs = time.perf_counter() - t0
         self.entries[key] = {"config": asdict(best), "best_ms": report["best_ms"],
                              "space_size": report["space_size"], "tuning_time_s": secs,
-                             "n_correct": sum(1 for r in report["results"] if r["correct"])}
+                             "n_correct": report["n_correct"], "n_unsupported": report["n_unsupported"],
+                             "n_incorrect": report["n_incorrect"], "gate": GATE_VERSION}
         return best, secs, False

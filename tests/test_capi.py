@@ -58,7 +58,7 @@ def test_unsupported_status_code():
     d.outputs = ["Y"]
     with pytest.raises(TaskmapError) as e:
         Plan(d)
-    assert e.value.status == 2  # usage: the DAG is valid but not a sum-reduction anchor
+    assert e.value.status == 4  # TM_ERR_UNSUPPORTED: a valid DAG whose anchor is not a sum reduction
 
 
 def test_product_never_imports_oracle():

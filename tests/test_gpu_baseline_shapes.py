@@ -1,0 +1,152 @@
+"""Oracle parity at the BASELINE shapes with the schedules the bench actually runs.
+
+For every workload key of tuning_cache.json (the configs bench.py binds), the
+cached ScheduleConfig is bound on that workload's real geometry at a reduced
+batch -- ResNet-50 convs with their true C/H/F/k/s/p at 1-2 images in the bench's
+channels-last layout (NHWC8 for conv1), the BERT FFN at 768/3072 on 128 tokens,
+attention at 128 x 64 on 4 heads -- and compared with the oracle port (pinned to
+reference_eval by tests/golden): exact on the reference's integer test data
+(bf16 outputs: equal to round_bf16 of the exact result), toleranced on floats.
+The whole schedule space is also swept over the FFN chain and one 3x3 conv.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import port
+from paper_2210_09603_b200 import Plan, ScheduleConfig, schedule_space, workloads as W
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _cache():
+    with open(os.path.join(ROOT, "tuning_cache.json")) as f:
+        return json.load(f)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _bf16(a):
+    t = _torch()
+    return t.from_numpy(np.ascontiguousarray(a, np.float32)).to(t.bfloat16).cuda()
+
+
+def _conv_case(L, n, cfg, seed):
+    """bench.build_sweep's layouts: channels-last X (NHWC8 for C < 8) and W, fp32
+    BN scale/shift, channels-last bf16 output."""
+    torch = _torch()
+    rng = port.Rng(seed)
+    x = rng.tensor((n, L.c, L.h, L.h), True)
+    wt = rng.tensor((L.f, L.c, L.k, L.k), True)
+    scale, shift = rng.tensor((L.f,), True), rng.tensor((L.f,), True)
+    if L.c < 8:
+        xb = torch.zeros((n, L.h, L.h, 8), dtype=torch.bfloat16, device="cuda")
+        xb[..., :L.c] = _bf16(x).permute(0, 2, 3, 1)
+        xd = xb.as_strided((n, L.c, L.h, L.h), (L.h * L.h * 8, 1, L.h * 8, 8))
+    else:
+        xd = _bf16(x).contiguous(memory_format=torch.channels_last)
+    wd = _bf16(wt).contiguous(memory_format=torch.channels_last)
+    ho = L.out_hw()
+    z = torch.full((n, L.f, ho, ho), float("nan"), dtype=torch.bfloat16, device="cuda").contiguous(
+        memory_format=torch.channels_last)
+    ins = [xd, wd, torch.from_numpy(scale.astype(np.float32)).cuda(), torch.from_numpy(shift.astype(np.float32)).cuda()]
+    ex = Plan(W.conv_bn_relu_dag(L, n), cfg).bind(ins, [z])
+    ex.launch()
+    torch.cuda.synchronize()
+    want = port.round_bf16(port.conv_bn_relu(x, wt, scale, shift, L.s, L.p))
+    return z.float().cpu().numpy().astype(np.float64), want
+
+
+CONV_KEYS = [(L, f"conv:{L.name}:b{W.RESNET_BATCH}:nhwc") for L in W.RESNET50]
+
+
+@pytest.mark.parametrize("L,key", CONV_KEYS, ids=[L.name for L, _ in CONV_KEYS])
+def test_tuned_conv_schedule_exact_at_layer_geometry(L, key):
+    cache = _cache()
+    if key not in cache:
+        pytest.skip(f"{key} not tuned")
+    cfg = ScheduleConfig(**cache[key]["config"])
+    n = 1 if L.h >= 56 else 2
+    got, want = _conv_case(L, n, cfg, seed=100 + W.RESNET50.index(L))
+    assert np.array_equal(got, want), f"{key} {cfg}"
+
+
+def _ffn(t, cfg, seed=91):
+    torch = _torch()
+    rng = port.Rng(seed)
+    dm, dff = W.BERT_HIDDEN, W.BERT_FFN
+    x, w1, b1 = (port.round_bf16(rng.tensor(s)) for s in ((t, dm), (dm, dff), (dff,)))
+    w2, b2 = port.round_bf16(rng.tensor((dff, dm))), port.round_bf16(rng.tensor((dm,)))
+    o = torch.full((t, dm), float("nan"), dtype=torch.bfloat16, device="cuda")
+    Plan(W.ffn_dag(t), cfg).bind([_bf16(a) for a in (x, w1, b1, w2, b2)], [o]).launch()
+    torch.cuda.synchronize()
+    got = o.float().cpu().numpy().astype(np.float64)
+    return got, (x, w1, b1, w2, b2)
+
+
+def _ffn_ok(got, args):
+    """bf16 H modelled: max_rel_error <= 2e-2 (SURVEY §8c chain tolerance); unmodelled,
+    relative to the output scale <= 1e-2 (tests/test_gpu_gemm.py::test_ffn_chain)."""
+    want_h = port.ffn(*args, round_h=port.round_bf16)
+    want = port.ffn(*args)
+    return (port.max_rel_error(got, want_h) <= 2e-2 and
+            np.abs(got - want).max() / np.abs(want).max() <= 1e-2)
+
+
+def test_tuned_ffn_schedule_at_bert_dims():
+    cache = _cache()
+    key = f"ffn:t{W.BERT_TOKENS}"
+    if key not in cache:
+        pytest.skip("ffn not tuned")
+    got, args = _ffn(128, ScheduleConfig(**cache[key]["config"]))
+    assert _ffn_ok(got, args)
+
+
+@pytest.mark.parametrize("which", ["qk", "pv"])
+def test_tuned_attention_schedule_exact(which):
+    torch = _torch()
+    cache = _cache()
+    key = f"attn.{which}:h{W.BERT_HEADS}"
+    if key not in cache:
+        pytest.skip(f"{key} not tuned")
+    cfg = ScheduleConfig(**cache[key]["config"])
+    h, s, d = 4, W.BERT_SEQ, W.BERT_HEAD_DIM
+    rng = port.Rng(93)
+    if which == "qk":
+        q, k = rng.tensor((h, s, d), True), rng.tensor((h, s, d), True)
+        out = torch.full((h, s, s), float("nan"), dtype=torch.bfloat16, device="cuda")
+        Plan(W.attention_scores_dag(h), cfg).bind([_bf16(q), _bf16(k)], [out]).launch()
+        want = port.round_bf16(port.batched_matmul_scale(q, k.transpose(0, 2, 1), 0.125))
+    else:
+        pm, v = rng.tensor((h, s, s), True), rng.tensor((h, s, d), True)
+        out = torch.full((h, s, d), float("nan"), dtype=torch.bfloat16, device="cuda")
+        Plan(W.attention_context_dag(h), cfg).bind([_bf16(pm), _bf16(v)], [out]).launch()
+        want = port.round_bf16(port.batched_matmul_scale(pm, v, 1.0))
+    torch.cuda.synchronize()
+    assert np.array_equal(out.float().cpu().numpy().astype(np.float64), want)
+
+
+def test_whole_space_ffn_chain():
+    """every config of the space is correct on the FFN chain."""
+    bad = []
+    for i, cfg in enumerate(schedule_space("matmul")):
+        got, args = _ffn(128, cfg, seed=95)
+        if not _ffn_ok(got, args):
+            bad.append((i, cfg))
+    assert not bad, bad
+
+
+def test_whole_space_3x3_conv_exact():
+    L = next(x for x in W.RESNET50 if x.name == "l3.c2")
+    bad = []
+    for i, cfg in enumerate(schedule_space("conv2d")):
+        got, want = _conv_case(L, 1, cfg, seed=97)
+        if not np.array_equal(got, want):
+            bad.append((i, cfg, int((got != want).sum())))
+    assert not bad, bad
