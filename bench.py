@@ -1,21 +1,28 @@
 #!/usr/bin/env python
 """Benchmark of the fused task-mapped GEMM / implicit-GEMM conv path on B200.
 
-One step = one batch-sharded sweep of BASELINE.json configs[4] on every rank:
+One step = one batch-sharded sweep of BASELINE.json configs[4]:
   * the 53 ResNet-50 conv layers as implicit GEMM with the
-    fused BN-fold + ReLU epilogue, batch 32 per GPU, bf16, channels-last;
-  * the BERT-base FFN chain (8192 tokens = batch 64 x seq 128, 768->3072 GELU
-    ->768 + residual), bf16;
-  * the BERT-base attention batched matmuls (12x16 = 192 heads, seq 128, d 64):
-    S = 0.125 Q K^T and O = S V, bf16;
+    fused BN-fold + ReLU epilogue, bf16, channels-last;
+  * the BERT-base FFN chain (768->3072 GELU ->768 + residual), bf16;
+  * the BERT-base attention batched matmuls (seq 128, d 64): S = 0.125 Q K^T and
+    O = S V, bf16;
 then the step's result tensors are gathered to rank 0 (the only collective).
-value = algorithmic FLOPs of all ranks / max-over-ranks step time (weak scaling).
+
+Scaling: strong by default -- the global batch of 32 images, 8192
+tokens (batch 64 x seq 128) and 192 heads (12 x 16) is split over the N ranks
+(identical weights on every rank); --scaling weak keeps that batch per GPU.
+value = algorithmic FLOPs of all ranks / max-over-ranks step time.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+With --gpus N > 1 and no torchrun environment, bench.py launches its own N
+ranks (python -m torch.distributed.run, one process per GPU).
 """
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -26,9 +33,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "fused GEMM/conv TFLOP/s & % tensor peak at 1/2/4/8 B200 vs ref CPU"
+SEED_WEIGHTS = 1234  # identical on every rank
 
 
 def peaks():
+    """(bf16 dense TFLOP/s, HBM GB/s, source) from the driver-written MEASURED_PEAKS.json."""
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         with open(p) as f:
@@ -90,21 +99,26 @@ class ClockSampler:
 
 # ---------------------------------------------------------------- workload --
 def cfg_str(cfg):
-    return f"bm{cfg.block_m}/bn{cfg.block_n}/sk{cfg.split_k}/{'deep' if cfg.pipeline else 'db'}/r{cfg.raster}"
+    return f"bm{cfg.block_m}/bn{cfg.block_n}/sk{cfg.split_k}/{'deep' if cfg.pipeline else 'db'}/r{cfg.raster}" + \
+        (f"/g{cfg.grid}" if cfg.grid else "")
 
 
-def build_sweep(torch, device, seed=0, tuner=None, tune_mode="auto", log=None):
-    """Allocates inputs/weights/outputs of one sweep and binds the fused plans.
-    Each distinct workload is tuned over schedule_space on the device (or its
-    cached best config is reused); returns (items, tuning report)."""
+def build_sweep(torch, device, shard, tuner=None, tune_mode="auto", log=None):
+    """Allocates this rank's inputs / weights / outputs of one sweep step and binds
+    the fused plans.  Weights come from one seed on every rank; activations from a
+    rank-specific stream (the rank's batch slice).  Each distinct per-GPU workload
+    is tuned over schedule_space on the device, or its cached best config reused.
+    Returns (items, tuning report)."""
     from paper_2210_09603_b200 import Plan, ScheduleConfig, workloads as W
 
-    g = torch.Generator(device=device)
-    g.manual_seed(seed)
+    gw = torch.Generator(device=device)
+    gw.manual_seed(SEED_WEIGHTS)
+    ga = torch.Generator(device=device)
+    ga.manual_seed(SEED_WEIGHTS + 7919 * (1 + shard.rank))
     treport = {"tuned": 0, "cached": 0, "seconds": 0.0, "configs": {}}
 
-    def rnd(shape, dtype=torch.bfloat16, cl=False):
-        t = torch.empty(shape, device=device, dtype=torch.float32).uniform_(-1, 1, generator=g).to(dtype)
+    def rnd(shape, dtype=torch.bfloat16, cl=False, gen=ga):
+        t = torch.empty(shape, device=device, dtype=torch.float32).uniform_(-1, 1, generator=gen).to(dtype)
         return t.contiguous(memory_format=torch.channels_last) if cl else t
 
     def conv_input(L, B):
@@ -125,17 +139,17 @@ def build_sweep(torch, device, seed=0, tuner=None, tune_mode="auto", log=None):
             log(f"{key}: {treport['configs'][key]} ({'cached' if cached else f'tuned in {secs:.1f}s'})")
         return cfg
 
-    items = []  # (name, group, flops, exec, inputs(list), outputs(list), result?)
-    B = W.RESNET_BATCH
+    items = []
+    B = shard.count("images")
     for L in W.RESNET50:
         dag = W.conv_bn_relu_dag(L, B)
         ho = L.out_hw()
         plan = None
         for rep in range(L.count):
             x = conv_input(L, B)
-            w = rnd((L.f, L.c, L.k, L.k), cl=True)
-            scale = rnd((L.f,), torch.float32)
-            shift = rnd((L.f,), torch.float32)
+            w = rnd((L.f, L.c, L.k, L.k), cl=True, gen=gw)
+            scale = rnd((L.f,), torch.float32, gen=gw)
+            shift = rnd((L.f,), torch.float32, gen=gw)
             z = torch.empty((B, L.f, ho, ho), device=device, dtype=torch.bfloat16).contiguous(
                 memory_format=torch.channels_last)
             if plan is None:
@@ -143,32 +157,38 @@ def build_sweep(torch, device, seed=0, tuner=None, tune_mode="auto", log=None):
                 cfg = pick(f"conv:{L.name}:b{B}:nhwc", dag, [x, w, scale, shift], [z], default)
                 plan = Plan(dag, cfg)
             ex = plan.bind([x, w, scale, shift], [z])
+            m, n, k = L.gemm(B)
             items.append(dict(name=f"{L.name}#{rep}", group="conv", flops=L.flops(B), exec=ex, inputs=[x],
-                              outputs=[z], plan=plan, cfg=cfg_str(cfg)))
+                              outputs=[z], plan=plan, cfg=cfg_str(cfg), weights=[w, scale, shift],
+                              ai_bytes=sum(t.numel() * t.element_size() for t in (x, w, scale, shift, z))))
+    items[-1]["result"] = True  # last conv layer (l4.ds) output
     # FFN chain
-    T = W.BERT_TOKENS
+    T = shard.count("tokens")
     dag = W.ffn_dag(T)
     x = rnd((T, W.BERT_HIDDEN))
-    ffn_in = [x, rnd((W.BERT_HIDDEN, W.BERT_FFN)), rnd((W.BERT_FFN,)), rnd((W.BERT_FFN, W.BERT_HIDDEN)),
-              rnd((W.BERT_HIDDEN,))]
+    wts = [rnd((W.BERT_HIDDEN, W.BERT_FFN), gen=gw), rnd((W.BERT_FFN,), gen=gw),
+           rnd((W.BERT_FFN, W.BERT_HIDDEN), gen=gw), rnd((W.BERT_HIDDEN,), gen=gw)]
+    ffn_in = [x] + wts
     o = torch.empty((T, W.BERT_HIDDEN), device=device, dtype=torch.bfloat16)
     plan = Plan(dag, pick(f"ffn:t{T}", dag, ffn_in, [o], ScheduleConfig(block_m=256, block_n=256)))
     items.append(dict(name="bert.ffn", group="ffn", flops=2.0 * T * W.BERT_HIDDEN * W.BERT_FFN * 2,
-                      exec=plan.bind(ffn_in, [o]), inputs=[x], outputs=[o], plan=plan, result=True))
-    # attention batched matmuls
-    H, S, D = W.BERT_HEADS, W.BERT_SEQ, W.BERT_HEAD_DIM
+                      exec=plan.bind(ffn_in, [o]), inputs=[x], outputs=[o], plan=plan, result=True, weights=wts,
+                      ai_bytes=sum(t.numel() * t.element_size() for t in ffn_in + [o])))
+    # attention batched matmuls (activations only: Q, K, V are per-token projections)
+    H, S, D = shard.count("heads"), W.BERT_SEQ, W.BERT_HEAD_DIM
     q, k, v = rnd((H, S, D)), rnd((H, S, D)), rnd((H, S, D))
     s = torch.empty((H, S, S), device=device, dtype=torch.bfloat16)
     dag1 = W.attention_scores_dag(H)
     p1 = Plan(dag1, pick(f"attn.qk:h{H}", dag1, [q, k], [s], ScheduleConfig(block_n=128)))
     items.append(dict(name="bert.qk", group="attn", flops=2.0 * H * S * S * D, exec=p1.bind([q, k], [s]),
-                      inputs=[q, k], outputs=[s], plan=p1))
+                      inputs=[q, k], outputs=[s], plan=p1, weights=[],
+                      ai_bytes=sum(t.numel() * t.element_size() for t in (q, k, s))))
     oc = torch.empty((H, S, D), device=device, dtype=torch.bfloat16)
     dag2 = W.attention_context_dag(H)
     p2 = Plan(dag2, pick(f"attn.pv:h{H}", dag2, [s, v], [oc], ScheduleConfig(block_n=64)))
     items.append(dict(name="bert.pv", group="attn", flops=2.0 * H * S * S * D, exec=p2.bind([s, v], [oc]),
-                      inputs=[v], outputs=[oc], plan=p2, result=True))
-    items[52]["result"] = True  # last conv layer (l4.ds) output
+                      inputs=[v], outputs=[oc], plan=p2, result=True, weights=[],
+                      ai_bytes=sum(t.numel() * t.element_size() for t in (s, v, oc))))
     return items, treport
 
 
@@ -176,42 +196,38 @@ def sweep_flops(items):
     return sum(it["flops"] for it in items)
 
 
-def algorithmic_bytes(it):
-    """compulsory bytes of one launch: inputs read once + outputs written once."""
-    n = 0
-    for t in it["exec"]._keep[0] + it["exec"]._keep[1]:
-        n += t.numel() * t.element_size()
-    return n
-
-
 # ----------------------------------------------------------- CPU reference --
 def cpu_sample_tasks():
-    """A bounded sample of the same sweep for the reference CPU interpreter:
-    conv layers on one image and 8 filters, FFN on 2 tokens, one attention head.
-    Returns [(dag_json, inputs, out_shapes, flops, port_fn)]."""
-    from oracle import port
-    from paper_2210_09603_b200 import workloads as W
+    """A bounded sample of the same sweep for the reference CPU interpreter, built
+    with the reference's own builders (oracle.ref_dags -> oracle/_ref), never the
+    product library: 6 conv layers on one image and 8 filters, the FFN on 2
+    tokens, one attention head.  Returns [(dag_json, inputs, out_shapes, flops, port_fn)]."""
+    from oracle import port, ref_dags
 
     rng = port.Rng(99)
     tasks = []
-    for L in [W.RESNET50[i] for i in (3, 9, 15, 20, 21, 16)]:
-        dag = W.conv_bn_relu_dag(L, 1, f=8)
-        ho = L.out_hw()
-        ins = {"X": rng.tensor((1, L.c, L.h, L.h)), "W": rng.tensor((8, L.c, L.k, L.k)),
-               "Scale": rng.tensor((8,)), "Shift": rng.tensor((8,))}
-        fn = (lambda ins=ins, L=L: port.conv_bn_relu(ins["X"], ins["W"], ins["Scale"], ins["Shift"], L.s, L.p))
-        tasks.append((dag.to_json(), ins, {"Z": (1, 8, ho, ho)}, 2.0 * ho * ho * 8 * L.c * L.k * L.k, fn))
+    # (name, C, H, k, s, p) of l1.c2, l2.c2, l3.c2, l4.c2s, l4.c1, l3.c3 (SURVEY App. B)
+    for _, c, h, k, s, p in (("l1.c2", 64, 56, 3, 1, 1), ("l2.c2", 128, 28, 3, 1, 1), ("l3.c2", 256, 14, 3, 1, 1),
+                             ("l4.c2s", 512, 14, 3, 2, 1), ("l4.c1", 2048, 7, 1, 1, 0), ("l3.c3", 256, 14, 1, 1, 0)):
+        f = 8
+        ho = (h + 2 * p - k) // s + 1
+        dag = ref_dags.conv_bn_relu(1, c, h, f, k, s, p)
+        ins = {"X": rng.tensor((1, c, h, h)), "W": rng.tensor((f, c, k, k)), "Scale": rng.tensor((f,)),
+               "Shift": rng.tensor((f,))}
+        fn = (lambda ins=ins, s=s, p=p: port.conv_bn_relu(ins["X"], ins["W"], ins["Scale"], ins["Shift"], s, p))
+        tasks.append((dag, ins, {"Z": (1, f, ho, ho)}, 2.0 * ho * ho * f * c * k * k, fn))
     t = 2
-    dag = W.ffn_dag(t)
     ins = {"X": rng.tensor((t, 768)), "W1": rng.tensor((768, 3072)), "b1": rng.tensor((3072,)),
            "W2": rng.tensor((3072, 768)), "b2": rng.tensor((768,))}
     fn = (lambda ins=ins: port.ffn(ins["X"], ins["W1"], ins["b1"], ins["W2"], ins["b2"]))
-    tasks.append((dag.to_json(), ins, {"O": (t, 768)}, 2.0 * t * 768 * 3072 * 2, fn))
-    dag = W.attention_scores_dag(1)
+    tasks.append((ref_dags.ffn(t), ins, {"O": (t, 768)}, 2.0 * t * 768 * 3072 * 2, fn))
     ins = {"Q": rng.tensor((1, 128, 64)), "K": rng.tensor((1, 128, 64))}
     fn = (lambda ins=ins: 0.125 * port.matmul(ins["Q"][0], ins["K"][0].T))
-    tasks.append((dag.to_json(), ins, {"S": (1, 128, 128)}, 2.0 * 128 * 128 * 64, fn))
+    tasks.append((ref_dags.attention_scores(1), ins, {"S": (1, 128, 128)}, 2.0 * 128 * 128 * 64, fn))
     return tasks
+
+
+CPU_SAMPLE = "6 ResNet-50 conv layers (1 image, 8 filters) + FFN (2 tokens) + 1 attention head"
 
 
 def run_cpu_sample(tasks, threads):
@@ -246,6 +262,64 @@ def traffic_of(group):
         return None
 
 
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def self_launch(args):
+    """--gpus N > 1 outside torchrun: run N ranks of this script, one per GPU."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+# ------------------------------------------------------------------ config 1 --
+def config1_lines(torch, device, peak_tf, sm_mhz, reps=50):
+    """BASELINE configs[0]: M=N=K=1024 matmul + fused bias + ReLU, fp32 semantics,
+    on the task-mapped CUDA-core kernel (math fp32_simt, the paper's
+    spatial(4,2)*repeat(2,2)*spatial(4,8)*repeat(4,4) mapping, PAPER.md:528-529),
+    plus the tf32 and bf16 tensor-core forms of the same problem."""
+    from paper_2210_09603_b200 import Graph, Plan, ScheduleConfig, workloads as W
+    m = n = k = 1024
+    g = torch.Generator(device=device)
+    g.manual_seed(11)
+    r = lambda *s, dt=torch.float32: torch.empty(s, device=device).uniform_(-1, 1, generator=g).to(dt)  # noqa: E731
+    flops = 2.0 * m * n * k
+    clk = (sm_mhz or 1965.0) / 1e3
+    ffma_peak = 148 * 128 * 2 * clk / 1e3  # TFLOP/s: 148 SMs x 128 FP32 lanes x FMA
+    out = {}
+    for name, dt, math, peak, peak_src in (
+            ("fp32_simt", torch.float32, "fp32_simt", ffma_peak, f"FFMA: 148 SM x 128 lanes x 2 x {clk:.3f} GHz"),
+            ("tf32", torch.float32, "tf32", peak_tf / 2, "kind::tf32 = half the measured bf16 dense peak"),
+            ("bf16", torch.bfloat16, "bf16", peak_tf, "measured bf16 dense peak")):
+        a, b, bias = r(m, k, dt=dt), r(k, n, dt=dt), r(n)
+        d = torch.empty((m, n), device=device, dtype=torch.float32)
+        best = None
+        for cfg in ([ScheduleConfig(math=math)] if math == "fp32_simt" else
+                    [ScheduleConfig(math=math, block_n=bn, split_k=sk) for bn in (128, 256) for sk in (1, 2, 4)]):
+            ex = Plan(W.matmul_bias_relu_dag(m, n, k), cfg).bind([a, b, bias], [d])
+            gr = Graph([ex] * reps)
+            gr.launch()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            gr.launch()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            if best is None or ms < best[0]:
+                best = (ms, cfg_str(cfg))
+        ms, cs = best
+        tf = flops / (ms / 1e3) / 1e12
+        out[name] = {"ms": round(ms, 5), "tflops": round(tf, 2), "schedule": cs,
+                     "roofline": {"bound": "fp32 FFMA" if math == "fp32_simt" else "tensor", "achieved": round(tf, 2),
+                                  "peak": round(peak, 1), "unit": "TFLOP/s", "frac": round(tf / peak, 4),
+                                  "peak_source": peak_src}}
+    return out
+
+
 # -------------------------------------------------------------------- main --
 def main():
     ap = argparse.ArgumentParser()
@@ -253,8 +327,10 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-config1", action="store_true")
     ap.add_argument("--tune", default="auto", choices=["auto", "force", "off"],
                     help="auto: reuse tuning_cache.json entries, tune the rest on the device")
     ap.add_argument("--tuning-cache", default=os.path.join(ROOT, "tuning_cache.json"))
@@ -264,12 +340,17 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
+
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     threads = args.cpu_threads or os.cpu_count() or 1
 
     if args.impl == "reference":
+        # the reference's own CPU implementation (oracle/_ref: reference builders +
+        # reference_eval), all host threads, rank 0 only; the product library is never loaded
         if rank != 0:
             return
         tasks = cpu_sample_tasks()
@@ -282,20 +363,21 @@ def main():
             fl += f
             secs += s
         value = fl / secs / 1e12
-        sample = "per step: 6 ResNet-50 conv layers (1 image, 8 filters) + FFN (2 tokens) + 1 attention head"
         print(json.dumps({
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": "configs[4] sweep sample on host CPU (taskmap::reference_eval)",
+            "config": {"workload": "configs[4] sweep sample on host CPU (taskmap::reference_eval, reference builders)",
                        "threads": threads},
-            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": kind, "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": threads, "kind": kind, "sample": CPU_SAMPLE},
             "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         }))
         return
 
     import torch
+    if world > torch.cuda.device_count():
+        raise SystemExit(f"bench.py: {world} ranks but only {torch.cuda.device_count()} visible GPUs")
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     dist = None
@@ -303,12 +385,12 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=device)
 
+    from paper_2210_09603_b200.sharding import gather_buffers, gather_to_root, sweep_shard
     from paper_2210_09603_b200.tuning import TuningCache
-    tuner = TuningCache(args.tuning_cache if rank == 0 else None)
-    if rank != 0 and os.path.exists(args.tuning_cache):
-        tuner = TuningCache(args.tuning_cache)  # read-only on other ranks
+    shard = sweep_shard(rank, world, args.scaling)
+    tuner = TuningCache(args.tuning_cache)
     t_build = time.perf_counter()
-    items, treport = build_sweep(torch, device, seed=1234 + rank, tuner=tuner, tune_mode=args.tune,
+    items, treport = build_sweep(torch, device, shard, tuner=tuner, tune_mode=args.tune,
                                  log=(lambda m: print(m, file=sys.stderr)) if rank == 0 else None)
     t_build = time.perf_counter() - t_build
     if rank == 0 and treport["tuned"]:
@@ -316,22 +398,21 @@ def main():
     flops_rank = sweep_flops(items)
     stream = torch.cuda.current_stream()
     results = [t for it in items if it.get("result") for t in it["outputs"]]
-    from paper_2210_09603_b200.sharding import gather_buffers, gather_to_root
-    gather_bufs = gather_buffers(results) if dist is not None else None
+    units = {"conv": "images", "ffn": "tokens", "attn": "heads"}
+    rows = [shard.sizes(units[it["group"]]) for it in items if it.get("result") for _ in it["outputs"]]
+    gather_bufs = gather_buffers(results, 0, [max(r) for r in rows]) if dist is not None else None
 
-    # the whole sweep replays as one CUDA graph (no per-kernel host launch cost);
-    # a second, timed graph with an event around every exec gives the per-launch
-    # breakdown (measured separately so its event nodes do not perturb `value`)
+    # the whole sweep replays as one CUDA graph (no per-kernel host launch cost)
     from paper_2210_09603_b200 import Graph
     graph = Graph([it["exec"] for it in items])
-    tgraph = Graph([it["exec"] for it in items], timed=True)
+    group_graphs = {g: Graph([it["exec"] for it in items if it["group"] == g]) for g in units}
 
     def step():
         graph.launch(stream)
 
     def gather():
         if dist is not None:
-            gather_to_root(results, 0, gather_bufs)
+            gather_to_root(results, 0, gather_bufs, rows)
 
     if args.launch_list:
         step()
@@ -344,36 +425,44 @@ def main():
         gather()
     torch.cuda.synchronize()
 
-    # ---- timed region: K steps, clocks sampled
+    def timed(fn, reps):
+        """device time per rep of fn() on `stream`, max over ranks (ms)"""
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        if dist is not None:
+            tt = torch.tensor([ms], device=device)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        return ms
+
+    # ---- timed region: K steps (sweep + final gather), clocks sampled
     clk = ClockSampler(local)
     clk.start()
     time.sleep(0.3)
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for s in range(args.steps):
-        step()
-        gather()
-    t1.record(stream)
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
+    ms = timed(lambda: (step(), gather()), args.steps)
     clocks = clk.stop()
-    ms = t0.elapsed_time(t1) / args.steps
-    if dist is not None:
-        tt = torch.tensor([ms], device=device)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
-    # ---- per-launch breakdown: the timed graph, K more steps
-    per_item = [0.0] * len(items)
-    for s in range(args.steps):
-        tgraph.launch(stream)
-        torch.cuda.synchronize()
-        for i, t in enumerate(tgraph.exec_ms()):
-            per_item[i] += t / args.steps
+    # compute only (no gather) and per kernel group, each replayed as its own graph
+    # (no event nodes between launches, so the group times add up to the sweep)
+    compute_ms = timed(step, args.steps)
+    group_ms = {g: timed(lambda gg=gg: gg.launch(stream), args.steps) for g, gg in group_graphs.items()}
+
+    per_item = None
+    if args.per_item and rank == 0:
+        tgraph = Graph([it["exec"] for it in items], timed=True)
+        per_item = [0.0] * len(items)
+        for _ in range(args.steps):
+            tgraph.launch(stream)
+            torch.cuda.synchronize()
+            for i, t in enumerate(tgraph.exec_ms()):
+                per_item[i] += t / args.steps
 
     # ---- e2e through the C ABI with host buffers: H2D inputs, launch, D2H results
     host_in = [[t.cpu().pin_memory() for t in it["inputs"]] for it in items]
@@ -381,13 +470,12 @@ def main():
                 for it in items]
     h2d = sum(t.numel() * t.element_size() for ts in host_in for t in ts)
     d2h = sum(t.numel() * t.element_size() for ts in host_out for t in ts)
-
-    # inputs stream in on a copy stream; each workload's kernels start as soon
-    # as its own inputs have landed, so H2D of later layers overlaps compute
     copy_stream = torch.cuda.Stream(device=device)
     in_ready = [torch.cuda.Event() for _ in items]
 
     def e2e_step():
+        # inputs stream in on a copy stream; each workload's kernels start as soon as
+        # its own inputs have landed, so H2D of later layers overlaps compute
         copy_stream.wait_stream(stream)  # the previous step is done reading these buffers
         with torch.cuda.stream(copy_stream):
             for ev, it, hin in zip(in_ready, items, host_in):
@@ -404,21 +492,11 @@ def main():
     for _ in range(2):
         e2e_step()
     torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e2e_steps = max(2, min(args.steps, 5))
-    if dist is not None:
-        dist.barrier()
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        e2e_step()
-    e1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1) / e2e_steps
-    if dist is not None:
-        tt = torch.tensor([e2e_ms], device=device)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
+    e2e_ms = timed(e2e_step, max(2, min(args.steps, 5)))
+
+    c1 = None
+    if rank == 0 and not args.no_config1:
+        c1 = config1_lines(torch, device, peaks()[0], clocks.get("sm_mhz"))
 
     if rank != 0:
         dist.destroy_process_group()
@@ -429,28 +507,34 @@ def main():
     total_flops = flops_rank * world
     value = total_flops / (ms / 1e3) / 1e12
     groups = {}
-    for it, t in zip(items, per_item):
-        g = groups.setdefault(it["group"], {"flops": 0.0, "ms": 0.0, "bytes": 0, "launches": 0})
+    for it in items:
+        g = groups.setdefault(it["group"], {"flops": 0.0, "bytes": 0, "launches": 0, "sol_ms": 0.0, "hbm_sol_ms": 0.0})
         g["flops"] += it["flops"]
-        g["ms"] += t
-        g["bytes"] += algorithmic_bytes(it)
+        g["bytes"] += it["ai_bytes"]
         g["launches"] += it["exec"].num_launches
-    for g in groups.values():
+        t_tc, t_hbm = it["flops"] / (peak_tf * 1e12) * 1e3, it["ai_bytes"] / (peak_bw * 1e9) * 1e3
+        g["sol_ms"] += max(t_tc, t_hbm)
+        g["hbm_sol_ms"] += t_hbm if t_hbm > t_tc else 0.0
+    for name, g in groups.items():
+        g["ms"] = group_ms[name]
         g["tflops"] = g["flops"] / (g["ms"] / 1e3) / 1e12
-        g["frac_of_peak"] = g["tflops"] / peak_tf
-        g["ms_share"] = g["ms"] / sum(x["ms"] for x in groups.values())
+        g["gbs"] = g["bytes"] / (g["ms"] / 1e3) / 1e9
+        g["frac_of_tensor_peak"] = g["tflops"] / peak_tf
+        g["sol_frac"] = g["sol_ms"] / g["ms"]  # per-launch roofline min(tensor, AI x HBM), summed
+        g["bound"] = "hbm" if g["hbm_sol_ms"] > 0.5 * g["sol_ms"] else "tensor"
+        g["ms_share"] = g["ms"] / sum(group_ms.values())
     dom = max(groups, key=lambda k: groups[k]["ms"])
     dg = groups[dom]
-    if args.per_item:
-        # per launch: time, TFLOP/s, roofline lower bound max(flops/peak, bytes/bw), fraction of it
+    if per_item is not None:
         sol_total = 0.0
         for it, t in zip(items, per_item):
-            by = algorithmic_bytes(it)
+            by = it["ai_bytes"]
             sol = max(it["flops"] / (peak_tf * 1e12), by / (peak_bw * 1e9)) * 1e3
             sol_total += sol
             print(f"{it['name']:12s} {t * 1e3:8.1f} us  {it['flops'] / (t / 1e3) / 1e12:7.1f} TFLOP/s  "
-                  f"AI {it['flops'] / by:6.0f}  SOL {sol * 1e3:6.1f} us ({sol / t:5.1%})  {it.get('cfg', '')}", file=sys.stderr)
-        print(f"sum {sum(per_item) * 1e3:.1f} us, SOL {sol_total * 1e3:.1f} us", file=sys.stderr)
+                  f"AI {it['flops'] / by:6.0f}  SOL {sol * 1e3:6.1f} us ({sol / t:5.1%})  {it.get('cfg', '')}",
+                  file=sys.stderr)
+        print(f"sum {sum(per_item) * 1e3:.1f} us (event-timed), SOL {sol_total * 1e3:.1f} us", file=sys.stderr)
     launches = sum(it["exec"].num_launches for it in items)
 
     cpu = None
@@ -458,37 +542,48 @@ def main():
         tasks = cpu_sample_tasks()
         f, s, kind = run_cpu_sample(tasks, threads)
         cpu = {"value": f / s / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": kind,
-               "sample": "6 ResNet-50 conv layers (1 image, 8 filters) + FFN (2 tokens) + 1 attention head, "
-                         f"{s:.1f} s on {threads} host threads"}
+               "sample": f"{CPU_SAMPLE}, {s:.1f} s on {threads} host threads"}
+    B, T, H = shard.global_count("images"), shard.global_count("tokens"), shard.global_count("heads")
+    dom_bound = dg["bound"]
+    if dom_bound == "hbm":
+        roof = {"bound": "hbm", "achieved": dg["gbs"], "peak": peak_bw, "unit": "GB/s", "frac": dg["gbs"] / peak_bw}
+    else:
+        roof = {"bound": "tensor", "achieved": dg["tflops"], "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": dg["tflops"] / peak_tf}
+    roof.update({"traffic": traffic_of(dom), "kernel": f"tm_gemm_kernel ({dom} launches)",
+                 "algorithmic_bytes_per_launch": dg["bytes"] / max(1, dg["launches"]),
+                 "algorithmic_flops_per_launch": dg["flops"] / max(1, dg["launches"]),
+                 "group_ms": dg["ms"], "sol_frac": dg["sol_frac"],
+                 "peak_source": f"{peak_src} (MEASURED_PEAKS.json bf16_tflops / hbm_gbs)"})
     out = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "configs[4]: batch-sharded sweep = 53 ResNet-50 conv+BN+ReLU (batch 32/GPU) + "
-                               "BERT FFN chain (64x128 tokens/GPU) + BERT attention QK^T/PV (192 heads/GPU)",
-                   "per_gpu_batch": {"resnet": 32, "bert_tokens": 8192, "bert_heads": 192},
-                   "parallelism": f"batch-sharded x{world}, final gather to rank 0",
-                   "l2": "inputs larger than L2 (~1 GB of activations per step)",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": args.scaling,
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (uniform(-1,1), random-init weights)",
+        "config": {"workload": "configs[4]: batch-sharded sweep = 53 ResNet-50 conv+BN+ReLU + BERT FFN chain "
+                               "(768->3072 GELU->768 + residual) + BERT attention QK^T / PV",
+                   "global_batch": {"resnet_images": B, "bert_tokens": T, "bert_heads": H},
+                   "per_gpu_batch": {"resnet_images": shard.count("images"), "bert_tokens": shard.count("tokens"),
+                                     "bert_heads": shard.count("heads")},
+                   "parallelism": f"batch-sharded x{world} ({args.scaling} scaling), final gather to rank 0",
+                   "l2": "inputs larger than L2 (~1 GB of activations per step at N=1)",
                    "frac_of_peak": value / world / peak_tf,
+                   "compute_ms_per_step": compute_ms, "gather_ms_per_step": max(0.0, ms - compute_ms),
                    "tuning": {"mode": args.tune, "workloads_tuned": treport["tuned"],
                               "workloads_cached": treport["cached"],
                               "tuning_time_s": round(treport["seconds"], 2),
                               "setup_time_s": round(t_build, 2),
                               "space_size": len(schedule_space("matmul"))}},
-        "roofline": {"bound": "tensor", "kernel": f"tm_gemm_kernel ({dom} launches)",
-                     "achieved": dg["tflops"], "peak": peak_tf, "unit": "TFLOP/s",
-                     "frac": dg["tflops"] / peak_tf, "traffic": traffic_of(dom),
-                     "algorithmic_bytes_per_launch": dg["bytes"] / max(1, dg["launches"]),
-                     "peak_source": f"{peak_src} bf16 burst"},
+        "roofline": roof,
         "breakdown": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                       for k, v in groups.items()},
-        "e2e": {"value": total_flops / (e2e_ms / 1e3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms,
+        "e2e": {"value": total_flops / (e2e_ms / 1e3) / 1e12, "unit": "TFLOP/s", "h2d_bytes_per_step": h2d * world,
+                "d2h_bytes_per_step": d2h * world, "ms_per_step": e2e_ms,
                 "schedule": "per-workload C-ABI launches; H2D on a copy stream overlapping compute"},
         "gpu_launches": launches * args.steps,
-        "launch": "one CUDA graph per step (all fused kernels of the sweep)",
+        "launch": "one CUDA graph per step (all fused kernels of the sweep), programmatic dependent launch",
         "clocks": clocks,
         "cpu_baseline": cpu,
+        "config1": c1,
     }
     print(json.dumps(out))
     if dist is not None:

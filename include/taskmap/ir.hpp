@@ -63,6 +63,7 @@ template <class... Args>
 enum class DType { F32, I32 };
 const char* dtype_name(DType t);
 DType dtype_from_name(const std::string& s);
+inline bool is_float_dtype(DType t) { return t == DType::F32; }
 
 // floor semantics (Python-style) used by all index arithmetic
 int64_t floordiv(int64_t a, int64_t b);

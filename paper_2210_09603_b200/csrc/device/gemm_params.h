@@ -92,13 +92,25 @@ enum LoaderKind : int32_t {
                         // channels >= C masked to zero (no per-box TMA cost: 49 taps)
 };
 
+// An elementwise prologue op applied to every operand element the gather
+// loader reads (fuse_prologue: Fig. 11's A[99-i] -> C[99-i]*2.0,
+// or a ReLU producer): the same constant-operand kinds as the epilogue
+// (EPI_*_C, EPI_RELU, EPI_NEG, EPI_EXP, EPI_SQRT, EPI_GELU_TANH).
+struct PreOp {
+  int32_t kind;
+  float c;
+};
+constexpr int kMaxPreOps = 4;
+
 // A strided operand: element (row, k, batch) at
-//   (row / P) * s_hi + (row % P) * s_lo + k * s_k + batch * s_batch + offset
+//   (row / P) * s_hi + (row % P) * s_lo + k * s_k + batch * s_batch + offset,
+// optionally transformed by an arithmetic prologue (n_pre ops, in order).
 struct Strided {
   const void* ptr;
   int32_t dtype;
-  int32_t pad_;
+  int32_t n_pre;
   int64_t P, s_hi, s_lo, s_k, s_batch, offset;
+  PreOp pre[kMaxPreOps];
 };
 
 // Convolution geometry (reference conv2d_im2col_dag arguments) plus element

@@ -123,6 +123,43 @@ __device__ __forceinline__ uint32_t load_bits(const void* base, int64_t idx, int
   }
 }
 
+__device__ __forceinline__ float gelu_tanh(float x);
+
+// Arithmetic prologue: load one element as fp32, apply the ops, convert to the
+// MMA input format (tf32 bits, bf16 or fp16).
+template <bool TF32>
+__device__ __noinline__ uint32_t load_pre(const Strided& s, int64_t idx, bool f16) {
+  float v = s.dtype == DT_F32    ? __ldg(reinterpret_cast<const float*>(s.ptr) + idx)
+            : s.dtype == DT_BF16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(s.ptr)[idx])
+                                 : __half2float(reinterpret_cast<const __half*>(s.ptr)[idx]);
+  for (int i = 0; i < s.n_pre; ++i) {
+    const float c = s.pre[i].c;
+    switch (s.pre[i].kind) {
+      case EPI_ADD_C: v = v + c; break;
+      case EPI_SUB_C: v = v - c; break;
+      case EPI_RSUB_C: v = c - v; break;
+      case EPI_MUL_C: v = v * c; break;
+      case EPI_DIV_C: v = v / c; break;
+      case EPI_RDIV_C: v = c / v; break;
+      case EPI_MAX_C: v = fmaxf(v, c); break;
+      case EPI_MIN_C: v = fminf(v, c); break;
+      case EPI_RELU: v = fmaxf(v, 0.f); break;
+      case EPI_NEG: v = -v; break;
+      case EPI_EXP: v = __expf(v); break;
+      case EPI_SQRT: v = sqrtf(v); break;
+      case EPI_GELU_TANH: v = gelu_tanh(v); break;
+      default: break;
+    }
+  }
+  if (TF32) return __float_as_uint(v);
+  if (f16) {
+    __half h = __float2half_rn(v);
+    return *reinterpret_cast<unsigned short*>(&h);
+  }
+  __nv_bfloat16 h = __float2bfloat16_rn(v);
+  return *reinterpret_cast<unsigned short*>(&h);
+}
+
 // Store one 16-byte chunk (chunk index c of a 128-byte K row) of tile row r
 // into a SWIZZLE_128B K-major tile (the layout TMA would have produced).
 __device__ __forceinline__ void st_sw128(uint8_t* tile, int r, int c, uint4 v) {
@@ -159,7 +196,9 @@ __device__ __forceinline__ void gather_row_strided(uint8_t* tile, int r, const S
 #pragma unroll
     for (int j = 0; j < PER; ++j) {
       const int k = k0 + c * PER + j;
-      bits[j] = (row_ok && k < K) ? load_bits<TF32>(s.ptr, base + (int64_t)k * s.s_k, s.dtype, f16) : 0u;
+      bits[j] = !(row_ok && k < K) ? 0u
+                : s.n_pre ? load_pre<TF32>(s, base + (int64_t)k * s.s_k, f16)
+                          : load_bits<TF32>(s.ptr, base + (int64_t)k * s.s_k, s.dtype, f16);
     }
     st_sw128(tile, r, c, pack_chunk<TF32>(bits));
   }

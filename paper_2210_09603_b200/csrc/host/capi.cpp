@@ -465,9 +465,8 @@ tm_status tm_dag_eval(const char* dag_json, const tm_tensor* in, int32_t n_in, c
     const cudaStream_t s = static_cast<cudaStream_t>(stream);
     for (int i = 0; i < n_out; ++i) {
       const std::string& o = d.outputs[i];
-      if (!r->is_float(o)) fail_unsupported("tm_dag_eval: output '", o, "' is not a float tensor");
       if (tmb::ev::numel_of(out[i]) != r->numel(o)) fail("tm_dag_eval: output '", o, "' has the wrong size");
-      tmb::ev::launch_store(r->values(o), r->numel(o), out[i].data, out[i].dtype, out[i].rank,
+      tmb::ev::launch_store(r->values(o), r->is_float(o), r->numel(o), out[i].data, out[i].dtype, out[i].rank,
                             tmb::ev::shape_of(out[i]), s);
     }
     tmb::sync_with_timeout(s, 60.0, "tm_dag_eval");

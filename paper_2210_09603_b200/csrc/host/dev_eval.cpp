@@ -139,7 +139,37 @@ void check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) fail_cuda(what, ": ", cudaGetErrorString(e));
 }
 
-bool expr_integer_exact(const Expr& e) {
+// value type of an expression under the interpreter's promotion rules
+// (compute_ir.cpp:277-366): float if a float immediate / f32 tensor / exp /
+// sqrt / cast feeds it through arithmetic; comparisons and logic are int
+bool expr_is_float(const ComputeDAG& dag, const Expr& e) {
+  switch (e->kind) {
+    case ExprKind::FloatImm: return true;
+    case ExprKind::IntImm:
+    case ExprKind::Var:
+    case ExprKind::ThreadIdx:
+    case ExprKind::BlockIdx:
+    case ExprKind::TableLookup: return false;
+    case ExprKind::Load: {
+      const TensorNode* t = dag.find(e->name);
+      return t != nullptr && t->dtype == DType::F32;
+    }
+    case ExprKind::Unary:
+      if (e->uop == UnOp::Exp || e->uop == UnOp::Sqrt || e->uop == UnOp::CastF32) return true;
+      if (e->uop == UnOp::CastI32) return false;
+      return expr_is_float(dag, e->args[0]);
+    case ExprKind::Select: return expr_is_float(dag, e->args[1]) || expr_is_float(dag, e->args[2]);
+    case ExprKind::Binary:
+      switch (e->bop) {
+        case BinOp::And: case BinOp::Or: case BinOp::Lt: case BinOp::Le: case BinOp::Gt: case BinOp::Ge:
+        case BinOp::Eq: case BinOp::Ne: return false;
+        default: return expr_is_float(dag, e->args[0]) || expr_is_float(dag, e->args[1]);
+      }
+  }
+  return false;
+}
+
+bool expr_integer_exact(const ComputeDAG& dag, const Expr& e) {
   switch (e->kind) {
     case ExprKind::FloatImm: {
       // exact in bf16 (8 significant bits): products with integers stay exact in fp32
@@ -152,13 +182,13 @@ bool expr_integer_exact(const Expr& e) {
     case ExprKind::Unary:
       if (e->uop == UnOp::Exp || e->uop == UnOp::Sqrt) return false;
       break;
-    case ExprKind::Binary:
-      if (e->bop == BinOp::Div) return false;
+    case ExprKind::Binary:  // float division (integer index division floors exactly)
+      if (e->bop == BinOp::Div && expr_is_float(dag, e)) return false;
       break;
     default: break;
   }
   for (const auto& a : e->args)
-    if (!expr_integer_exact(a)) return false;
+    if (!expr_integer_exact(dag, a)) return false;
   return true;
 }
 
@@ -166,7 +196,7 @@ bool expr_integer_exact(const Expr& e) {
 
 bool dag_integer_exact(const ComputeDAG& dag) {
   for (const auto& n : dag.nodes)
-    if (n.is_computed() && !expr_integer_exact(n.value)) return false;
+    if (n.is_computed() && !expr_integer_exact(dag, n.value)) return false;
   return true;
 }
 
@@ -266,10 +296,10 @@ DagEval::DagEval(const ComputeDAG& dag, const tm_tensor* inputs, int n_in, const
   if (err == 2) fail("device evaluator: float value stored to an i32 tensor");
 }
 
-const double* DagEval::values(const std::string& node) const {
+const void* DagEval::values(const std::string& node) const {
   auto it = dense_.find(node);
   if (it == dense_.end()) fail("device evaluator: '", node, "' is not a computed node");
-  return static_cast<const double*>(it->second.first->p);
+  return it->second.first->p;
 }
 
 int64_t DagEval::numel(const std::string& node) const {

@@ -29,10 +29,12 @@ void launch_fill(void* p, int32_t dt, int32_t rank, const TensorShape& s, int64_
                  cudaStream_t st);
 void launch_fill_nan(void* p, int32_t dt, int64_t span, cudaStream_t st);
 // dense fp64 values -> a strided tensor of any float dtype (round to nearest)
-void launch_store(const double* v, int64_t n, void* p, int32_t dt, int32_t rank, const TensorShape& s, cudaStream_t st);
+// (int64 values when !is_float: an i32 node of the DAG)
+void launch_store(const void* v, bool is_float, int64_t n, void* p, int32_t dt, int32_t rank, const TensorShape& s,
+                  cudaStream_t st);
 // host3 = {max error, #bit mismatches vs the rounded reference, scale (rms of the reference)}
-void launch_compare(const void* cand, int32_t dt, int32_t rank, const TensorShape& s, const double* ref, int64_t n,
-                    double* tmp3, double* host3, cudaStream_t st);
+void launch_compare(const void* cand, int32_t dt, int32_t rank, const TensorShape& s, const void* ref, bool is_float,
+                    int64_t n, double* tmp3, double* host3, cudaStream_t st);
 
 // Owns device memory released on destruction (RAII for the tuner's buffers).
 struct DeviceBuffer {
@@ -53,7 +55,8 @@ class DagEval {
  public:
   DagEval(const taskmap::ComputeDAG& dag, const tm_tensor* inputs, int n_in, const std::map<std::string, int>& round,
           cudaStream_t s);
-  const double* values(const std::string& node) const;  // dense row-major (float nodes)
+  // dense row-major values of a computed node: double (float nodes) or int64 (i32 nodes)
+  const void* values(const std::string& node) const;
   int64_t numel(const std::string& node) const;
   bool is_float(const std::string& node) const;
 

@@ -480,9 +480,66 @@ SubgraphPlan lower_subgraph(const ComputeDAG& dag, const FusedSubgraph& sg) {
         return;
       }
     }
-    if (!reindex(op.addr))
-      fail_unsupported("prologue '", s.name, "' is not a pure re-index of a graph input (arithmetic prologues are out of scope)");
     op.kind = OperandPlan::Strided;
+    if (reindex(op.addr)) return;
+    // Arithmetic prologue (Fig. 11: A[99-i] -> C[99-i]*2.0): the
+    // node's value is a chain of elementwise ops over ONE element of a graph input
+    // with constant side operands.  The input's index expressions are composed with
+    // the anchor's access (as for a re-index) and the chain becomes the operand's
+    // prologue op list, applied by the gather loader to every element it reads.
+    std::vector<Expr> lds;
+    collect_loads(s.value, lds);
+    if (lds.size() != 1 || dag.at(lds[0]->name).kind != NodeKind::Input)
+      fail_unsupported("prologue '", s.name, "' must read exactly one element of one graph input");
+    const Expr src = lds[0];
+    std::function<void(const Expr&)> chain = [&](const Expr& e) {
+      if (e->kind == ExprKind::Load) return;  // the source element
+      if (e->kind == ExprKind::Unary) {
+        chain(e->args[0]);
+        switch (e->uop) {
+          case UnOp::Relu: op.pre.push_back({EPI_RELU}); return;
+          case UnOp::Neg: op.pre.push_back({EPI_NEG}); return;
+          case UnOp::Exp: op.pre.push_back({EPI_EXP}); return;
+          case UnOp::Sqrt: op.pre.push_back({EPI_SQRT}); return;
+          case UnOp::CastF32: return;
+          default: fail_unsupported("prologue op ", unop_name(e->uop), " is not supported on the device");
+        }
+      }
+      if (e->kind == ExprKind::Binary) {
+        std::vector<Expr> l0, l1;
+        collect_loads(e->args[0], l0);
+        collect_loads(e->args[1], l1);
+        if (l0.empty() == l1.empty())
+          fail_unsupported("prologue expression is not a chain of its input element: ", expr_to_text(e));
+        const bool l = !l0.empty();
+        const Expr side = fold(l ? e->args[1] : e->args[0]);
+        if (side->kind != ExprKind::FloatImm && side->kind != ExprKind::IntImm)
+          fail_unsupported("prologue side operands must be constants: ", expr_to_text(side));
+        chain(l ? e->args[0] : e->args[1]);
+        EpiStep st{0};
+        st.c = static_cast<float>(side->kind == ExprKind::FloatImm ? side->fval : static_cast<double>(side->ival));
+        switch (e->bop) {
+          case BinOp::Add: st.kind = EPI_ADD_C; break;
+          case BinOp::Sub: st.kind = l ? EPI_SUB_C : EPI_RSUB_C; break;
+          case BinOp::Mul: st.kind = EPI_MUL_C; break;
+          case BinOp::Div: st.kind = l ? EPI_DIV_C : EPI_RDIV_C; break;
+          case BinOp::Max: st.kind = EPI_MAX_C; break;
+          case BinOp::Min: st.kind = EPI_MIN_C; break;
+          default: fail_unsupported("prologue operator ", binop_name(e->bop), " is not supported on the device");
+        }
+        op.pre.push_back(st);
+        return;
+      }
+      fail_unsupported("unsupported prologue expression: ", expr_to_text(e));
+    };
+    chain(s.value);
+    if (op.pre.size() > static_cast<size_t>(kMaxPreOps))
+      fail_unsupported("prologue '", s.name, "' has more than ", kMaxPreOps, " ops");
+    std::map<std::string, Expr> sub_map;
+    for (size_t d = 0; d < s.axes.size(); ++d) sub_map[s.axes[d].name] = idx[d];
+    op.addr.tensor = src->name;
+    op.addr.idx.clear();
+    for (const auto& i : src->args) op.addr.idx.push_back(fold(substitute(i, sub_map)));
   };
   lower_operand(ia, sp.a);
   lower_operand(ib, sp.b);
@@ -528,7 +585,9 @@ std::string SubgraphPlan::describe() const {
   auto opd = [&](const OperandPlan& p) {
     if (p.kind == OperandPlan::Im2col) return std::string("im2col(") + p.conv.x_tensor + ")";
     if (p.kind == OperandPlan::ConvFilter) return std::string("filter(") + p.conv.w_tensor + ")";
-    return idxs(p.addr);
+    std::string s = idxs(p.addr);
+    for (const auto& st : p.pre) s += " |> op" + std::to_string(st.kind) + "(" + std::to_string(st.c) + ")";
+    return s;
   };
   o << "{\"anchor\":" << tmjson::quote(sg.anchor) << ",\"M\":" << M << ",\"N\":" << N << ",\"K\":" << K
     << ",\"batch\":" << batch << ",\"A\":" << tmjson::quote(opd(a)) << ",\"B\":" << tmjson::quote(opd(b))
@@ -817,11 +876,13 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
     k.stages = plan.cfg.pipeline ? plan.cfg.stages : 2;
     p.num_kb = static_cast<int32_t>((sp.K + BK - 1) / BK);
     p.tiles_n = static_cast<int32_t>((sp.N + k.bn - 1) / k.bn);
-    auto strided_of = [&](const Fit& f, const tm_tensor& t) {
+    auto strided_of = [&](const Fit& f, const tm_tensor& t, const std::vector<EpiStep>& pre) {
       Strided s{};
       s.ptr = t.data;
       s.dtype = t.dtype;
       s.P = f.P; s.s_hi = f.hi; s.s_lo = f.lo; s.s_k = f.c1; s.s_batch = f.c2; s.offset = f.off;
+      s.n_pre = static_cast<int32_t>(pre.size());
+      for (size_t i = 0; i < pre.size() && i < static_cast<size_t>(kMaxPreOps); ++i) s.pre[i] = PreOp{pre[i].kind, pre[i].c};
       return s;
     };
     std::string why;
@@ -874,8 +935,8 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
     } else {
       Fit f;
       if (!fit_address(sp.a.addr, *opa, sp.M, sp.K, sp.batch, f, why)) fail_unsupported("operand A '", sp.a.addr.tensor, "': ", why);
-      p.a = strided_of(f, *opa);
-      if (tma_ok_kmajor(f, *opa, sp.M, want_dt, sp.batch)) {
+      p.a = strided_of(f, *opa, sp.a.pre);
+      if (sp.a.pre.empty() && tma_ok_kmajor(f, *opa, sp.M, want_dt, sp.batch)) {
         p.a_loader = LD_TMA_K;
         const uint64_t dims[3] = {(uint64_t)sp.K, (uint64_t)sp.M, (uint64_t)sp.batch};
         const uint64_t strides[2] = {(uint64_t)(f.lo * esize(opa->dtype)),
@@ -930,15 +991,15 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       if (sp.b.addr.idx.empty()) fail("operand B must be a strided tensor or a conv filter");
       Fit f;
       if (!fit_address(sp.b.addr, *opb, sp.N, sp.K, sp.batch, f, why)) fail_unsupported("operand B '", sp.b.addr.tensor, "': ", why);
-      p.b = strided_of(f, *opb);
-      if (tma_ok_kmajor(f, *opb, sp.N, want_dt, sp.batch)) {
+      p.b = strided_of(f, *opb, sp.b.pre);
+      if (sp.b.pre.empty() && tma_ok_kmajor(f, *opb, sp.N, want_dt, sp.batch)) {
         p.b_loader = LD_TMA_K;
         const uint64_t dims[3] = {(uint64_t)sp.K, (uint64_t)sp.N, (uint64_t)sp.batch};
         const uint64_t strides[2] = {(uint64_t)(f.lo * esize(opb->dtype)),
                                      (uint64_t)(std::max<int64_t>(f.c2, f.lo * sp.N) * esize(opb->dtype))};
         const uint32_t box[3] = {(uint32_t)BK, (uint32_t)bn_cta, 1u};
         make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * esize(opb->dtype), opb->dtype, 3, dims, strides, box);
-      } else if (!k.tf32 && bn_cta % 64 == 0 && tma_ok_mnmajor(f, *opb, sp.N, sp.K, sp.batch)) {
+      } else if (!k.tf32 && sp.b.pre.empty() && bn_cta % 64 == 0 && tma_ok_mnmajor(f, *opb, sp.N, sp.K, sp.batch)) {
         p.b_loader = LD_TMA_MN;
         if (sp.N % 64 == 0 && !std::getenv("TMB_NO_MN4D")) {
           // {64 n, K, N/64 n-blocks, batch}: one box per slot lands the BN/64 column
@@ -1084,6 +1145,12 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
     }
     if (const char* sw = std::getenv("TMB_MN_SWAP")) p.mn_lbo_sbo_swap = std::atoi(sw);
     p.fast_math = p.out_dtype != TM_F32;  // approximate tanh only where the output rounding dominates
+    // fault injection for the tuner-gate test (tests/test_gpu_tuner.py): every kernel
+    // silently drops its last k-block, so every schedule computes a wrong result
+    if (std::getenv("TMB_FAULT_SKIP_KBLOCK") && p.num_kb > 1) {
+      p.num_kb -= 1;
+      p.K = p.num_kb * BK;
+    }
     // split-K: every split gets a non-empty k-block range
     {
       int s = k.simt ? 1 : std::max(1, std::min(plan.cfg.split_k, p.num_kb));

@@ -39,16 +39,17 @@ struct ConvInfo {
   std::string x_tensor, w_tensor;
 };
 
-struct OperandPlan {
-  enum Kind { Strided, Im2col, ConvFilter } kind = Strided;
-  AddrExpr addr;  // Strided: physical idx in (row, k, batch)
-  ConvInfo conv;  // Im2col / ConvFilter
-};
-
 struct EpiStep {
   int32_t kind;   // tmb::EpiKind
   float c = 0.f;
   int side = -1;  // index into SubgraphPlan::sides for *_T kinds
+};
+
+struct OperandPlan {
+  enum Kind { Strided, Im2col, ConvFilter } kind = Strided;
+  AddrExpr addr;  // Strided: physical idx in (row, k, batch)
+  ConvInfo conv;  // Im2col / ConvFilter
+  std::vector<EpiStep> pre;  // arithmetic prologue (constant operands only), applied per loaded element
 };
 
 struct SubgraphPlan {

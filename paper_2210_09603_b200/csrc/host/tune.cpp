@@ -85,8 +85,6 @@ TuneOutcome tune(const ComputeDAG& d, const tm_tensor* in, int n_in, const tm_te
   d.validate();
   if (n_in != static_cast<int>(d.inputs.size()) || n_out != static_cast<int>(d.outputs.size()))
     fail("tune: expected ", d.inputs.size(), " inputs and ", d.outputs.size(), " outputs");
-  for (const auto& o : d.outputs)
-    if (d.at(o).dtype != taskmap::DType::F32) fail_unsupported("tune: output '", o, "' is not a float tensor");
   reps = std::max(reps, 1);
   Stream st;
   Event e0, e1;
@@ -138,8 +136,8 @@ TuneOutcome tune(const ComputeDAG& d, const tm_tensor* in, int n_in, const tm_te
     for (int i = 0; i < n_out; ++i) {
       double h[3];
       const tm_tensor& o = vout[t][i];
-      ev::launch_compare(o.data, o.dtype, o.rank, ev::shape_of(o), ref[t]->values(d.outputs[i]), ev::numel_of(o),
-                         static_cast<double*>(tmp3.p), h, s);
+      ev::launch_compare(o.data, o.dtype, o.rank, ev::shape_of(o), ref[t]->values(d.outputs[i]),
+                         ref[t]->is_float(d.outputs[i]), ev::numel_of(o), static_cast<double*>(tmp3.p), h, s);
       err = std::max(err, h[0]);
       nbad += h[1];
       tol = std::max(tol, tolerance(o.dtype));

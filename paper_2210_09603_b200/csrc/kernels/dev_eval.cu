@@ -252,7 +252,11 @@ __global__ void fill_values_kernel(void* p, int32_t dt, int32_t rank, TensorShap
   }
 }
 
-__global__ void store_kernel(const double* v, int64_t n, void* p, int32_t dt, int32_t rank, TensorShape s) {
+__device__ __forceinline__ double ref_value(const void* v, int64_t i, bool is_float) {
+  return is_float ? reinterpret_cast<const double*>(v)[i] : static_cast<double>(reinterpret_cast<const long long*>(v)[i]);
+}
+
+__global__ void store_kernel(const void* v, bool is_float, int64_t n, void* p, int32_t dt, int32_t rank, TensorShape s) {
   for (int64_t flat = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; flat < n;
        flat += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     int64_t rem = flat, off = 0;
@@ -260,7 +264,7 @@ __global__ void store_kernel(const double* v, int64_t n, void* p, int32_t dt, in
       off += (rem % s.shape[d]) * s.stride[d];
       rem /= s.shape[d];
     }
-    const double x = v[flat];
+    const double x = ref_value(v, flat, is_float);
     if (dt == TM_F32) reinterpret_cast<float*>(p)[off] = static_cast<float>(x);
     else if (dt == TM_BF16) reinterpret_cast<__nv_bfloat16*>(p)[off] = __double2bfloat16(x);
     else reinterpret_cast<__half*>(p)[off] = __double2half(x);
@@ -301,19 +305,21 @@ __device__ void atomic_max_double(double* a, double v) {
   }
 }
 
-__global__ void sumsq_kernel(const double* ref, int64_t n, double* out) {
+__global__ void sumsq_kernel(const void* ref, bool is_float, int64_t n, double* out) {
   double s = 0.0;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    s += ref[i] * ref[i];
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double x = ref_value(ref, i, is_float);
+    s += x * x;
+  }
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if ((threadIdx.x & 31) == 0) atomicAdd(out, s);
 }
 
 // out[0] = max error |c - r| / max(1, |r|, scale); out[1] = #elements whose bits
 // differ from the reference rounded to the output dtype (as a double)
-__global__ void compare_kernel(const void* cand, int32_t dt, int32_t rank, TensorShape s, const double* ref,
-                               double scale, double* out) {
+__global__ void compare_kernel(const void* cand, int32_t dt, int32_t rank, TensorShape s, const void* ref,
+                               bool is_float, double scale, double* out) {
   int64_t numel = 1;
   for (int d = 0; d < rank; ++d) numel *= s.shape[d];
   double emax = 0.0;
@@ -327,7 +333,7 @@ __global__ void compare_kernel(const void* cand, int32_t dt, int32_t rank, Tenso
     }
     uint32_t bits;
     const double c = phys_value(cand, dt, off, &bits);
-    const double r = ref[flat];
+    const double r = ref_value(ref, flat, is_float);
     const double den = fmax(1.0, fmax(fabs(r), scale));
     double e = fabs(c - r) / den;
     if (!(e == e)) e = INFINITY;  // NaN: never a match
@@ -377,22 +383,23 @@ void launch_fill_nan(void* p, int32_t dt, int64_t span, cudaStream_t st) {
   check(cudaGetLastError(), "fill kernel launch");
 }
 
-void launch_store(const double* v, int64_t n, void* p, int32_t dt, int32_t rank, const TensorShape& s, cudaStream_t st) {
+void launch_store(const void* v, bool is_float, int64_t n, void* p, int32_t dt, int32_t rank, const TensorShape& s,
+                  cudaStream_t st) {
   if (n <= 0) return;
-  store_kernel<<<grid_for(n), 256, 0, st>>>(v, n, p, dt, rank, s);
+  store_kernel<<<grid_for(n), 256, 0, st>>>(v, is_float, n, p, dt, rank, s);
   check(cudaGetLastError(), "store kernel launch");
 }
 
-void launch_compare(const void* cand, int32_t dt, int32_t rank, const TensorShape& s, const double* ref, int64_t n,
-                    double* tmp3, double* host3, cudaStream_t st) {
+void launch_compare(const void* cand, int32_t dt, int32_t rank, const TensorShape& s, const void* ref, bool is_float,
+                    int64_t n, double* tmp3, double* host3, cudaStream_t st) {
   check(cudaMemsetAsync(tmp3, 0, 3 * sizeof(double), st), "cudaMemsetAsync");
-  sumsq_kernel<<<grid_for(n), 256, 0, st>>>(ref, n, tmp3 + 2);
+  sumsq_kernel<<<grid_for(n), 256, 0, st>>>(ref, is_float, n, tmp3 + 2);
   check(cudaGetLastError(), "compare kernel launch");
   double h[3];
   check(cudaMemcpyAsync(h, tmp3, 3 * sizeof(double), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
   check(cudaStreamSynchronize(st), "compare synchronize");
   const double scale = n > 0 ? std::sqrt(h[2] / static_cast<double>(n)) : 0.0;
-  compare_kernel<<<grid_for(n), 256, 0, st>>>(cand, dt, rank, s, ref, scale, tmp3);
+  compare_kernel<<<grid_for(n), 256, 0, st>>>(cand, dt, rank, s, ref, is_float, scale, tmp3);
   check(cudaGetLastError(), "compare kernel launch");
   check(cudaMemcpyAsync(host3, tmp3, 2 * sizeof(double), cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
   check(cudaStreamSynchronize(st), "compare synchronize");

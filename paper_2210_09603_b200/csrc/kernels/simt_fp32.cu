@@ -40,6 +40,35 @@ __device__ __forceinline__ float ld_elem(const void* base, int64_t idx, int32_t 
   return __half2float(reinterpret_cast<const __half*>(base)[idx]);
 }
 
+// operand element with its arithmetic prologue applied (fuse_prologue)
+__device__ __forceinline__ float ld_operand(const Strided& s, int64_t idx) {
+  float v = ld_elem(s.ptr, idx, s.dtype);
+  for (int i = 0; i < s.n_pre; ++i) {
+    const float c = s.pre[i].c;
+    switch (s.pre[i].kind) {
+      case EPI_ADD_C: v = v + c; break;
+      case EPI_SUB_C: v = v - c; break;
+      case EPI_RSUB_C: v = c - v; break;
+      case EPI_MUL_C: v = v * c; break;
+      case EPI_DIV_C: v = v / c; break;
+      case EPI_RDIV_C: v = c / v; break;
+      case EPI_MAX_C: v = fmaxf(v, c); break;
+      case EPI_MIN_C: v = fminf(v, c); break;
+      case EPI_RELU: v = fmaxf(v, 0.f); break;
+      case EPI_NEG: v = -v; break;
+      case EPI_EXP: v = expf(v); break;
+      case EPI_SQRT: v = sqrtf(v); break;
+      case EPI_GELU_TANH: {
+        const float u = 0.7978845608028654f * (v + 0.044715f * v * v * v);
+        v = 0.5f * v * (1.0f + (1.0f - 2.0f / (expf(2.0f * u) + 1.0f)));
+        break;
+      }
+      default: break;
+    }
+  }
+  return v;
+}
+
 __device__ __forceinline__ int64_t row_part(int64_t P, int64_t hi, int64_t lo, int64_t r) {
   return (r / P) * hi + (r % P) * lo;
 }
@@ -103,7 +132,7 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const __grid_constant__ 
       LoadA::task(t, i, c);  // (m, k) within the tile
       const int64_t m = m0 + c[0], k = k0 + c[1];
       ra[i] = (m < p.M && k < p.K)
-                  ? ld_elem(A.ptr, row_part(A.P, A.s_hi, A.s_lo, m) + k * A.s_k + b * A.s_batch + A.offset, A.dtype)
+                  ? ld_operand(A, row_part(A.P, A.s_hi, A.s_lo, m) + k * A.s_k + b * A.s_batch + A.offset)
                   : 0.f;
     }
 #pragma unroll
@@ -112,7 +141,7 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const __grid_constant__ 
       LoadB::task(t, i, c);  // (k, n) within the tile
       const int64_t k = k0 + c[0], n = n0 + c[1];
       rb[i] = (n < p.N && k < p.K)
-                  ? ld_elem(B.ptr, row_part(B.P, B.s_hi, B.s_lo, n) + k * B.s_k + b * B.s_batch + B.offset, B.dtype)
+                  ? ld_operand(B, row_part(B.P, B.s_hi, B.s_lo, n) + k * B.s_k + b * B.s_batch + B.offset)
                   : 0.f;
     }
   };

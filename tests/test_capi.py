@@ -27,11 +27,17 @@ def test_header_symbols_all_exported():
         assert hasattr(lib, n), f"{n} declared in taskmap_b200.h but not exported"
 
 
-def test_only_tm_symbols_exported():
+def test_only_declared_symbols_exported():
+    """The library exports exactly the C ABI of include/taskmap_b200.h (extern "C" tm_*)
+    plus the C++ boundary in namespace taskmap (include/taskmap/*.hpp); nothing else."""
     out = subprocess.run(["nm", "-D", "--defined-only", pkg.lib_path()], capture_output=True, text=True).stdout
-    syms = [l.split()[-1] for l in out.splitlines() if " T " in l]
-    assert syms and all(s.startswith("tm_") for s in syms), [s for s in syms if not s.startswith("tm_")][:5]
-    assert sorted(syms) == declared()
+    syms = [l.split()[-1] for l in out.splitlines() if " T " in l or " W " in l]
+    c_syms = [s for s in syms if s.startswith("tm_")]
+    assert sorted(c_syms) == declared()
+    cxx = subprocess.run(["c++filt"], input="\n".join(s for s in syms if not s.startswith("tm_")),
+                         capture_output=True, text=True).stdout.split("\n")
+    cxx = [c for c in cxx if c]
+    assert cxx and all(c.startswith("taskmap::") or "taskmap::" in c.split("(")[0] for c in cxx), cxx[:5]
 
 
 def test_status_codes_and_last_error():

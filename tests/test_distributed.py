@@ -10,7 +10,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2210_09603_b200.sharding import gather_to_root, shard_range
+from paper_2210_09603_b200.sharding import shard_range
 
 
 def test_shard_range_partitions():
@@ -31,39 +31,67 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, q):
+def _worker(rank, world, port, q, scaling):
+    """One rank of bench.py's shard -> compute -> gather path (sharding.py), on CPU.
+    The per-rank compute stands in for the fused kernels (GPU-only): a conv whose
+    output is channels-last (the bench's layout) and a token-wise FFN-like map."""
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from oracle import port as P
-        # global batch of a BERT-style batched matmul (8 heads); identical weights on every rank
-        heads = 8
-        rng = P.Rng(42)
-        q_all = rng.tensor((heads, 16, 8))
-        k_all = rng.tensor((heads, 8, 16))
-        s, e = shard_range(heads, rank, world)
-        local = torch.from_numpy(P.batched_matmul_scale(q_all[s:e], k_all[s:e], 0.125))  # this rank's slice
-        got = gather_to_root([local])
+        from paper_2210_09603_b200.sharding import assemble, gather_buffers, gather_to_root, sweep_shard
+        totals = {"images": 5, "tokens": 37, "heads": 6}
+        shard = sweep_shard(rank, world, scaling, totals)
+        g = torch.Generator().manual_seed(7)  # weights: one seed, identical on every rank
+        w_conv, w_tok = torch.randn(4, 3, 3, 3, generator=g), torch.randn(8, 8, generator=g)
+        glob = {u: shard.global_count(u) for u in totals}
+        gx = torch.Generator().manual_seed(11)  # the global batch, sliced per rank
+        x_all, t_all = torch.randn(glob["images"], 3, 9, 9, generator=gx), torch.randn(glob["tokens"], 8, generator=gx)
+        if scaling == "weak":
+            assert shard.count("images") == totals["images"] and glob["images"] == totals["images"] * world
+        (i0, i1), (t0, t1) = shard.range("images"), shard.range("tokens")
+        y = torch.nn.functional.conv2d(x_all[i0:i1], w_conv, padding=1).contiguous(memory_format=torch.channels_last)
+        z = torch.relu(t_all[t0:t1] @ w_tok)
+        rows = [shard.sizes("images"), shard.sizes("tokens")]
+        bufs = gather_buffers([y, z], 0, [max(r) for r in rows])
+        got = gather_to_root([y, z], 0, bufs, rows)
         if rank == 0:
-            full = torch.cat(got[0], dim=0).numpy()
-            q.put(bool(np.array_equal(full, P.batched_matmul_scale(q_all, k_all, 0.125))))
+            want_y = torch.nn.functional.conv2d(x_all, w_conv, padding=1)
+            want_z = torch.relu(t_all @ w_tok)
+            # (CPU conv / matmul kernels may block differently per slice size: allclose, not bitwise)
+            q.put(bool(torch.allclose(assemble(got[0]), want_y, rtol=1e-5, atol=1e-5) and
+                       torch.allclose(assemble(got[1]), want_z, rtol=1e-5, atol=1e-5)))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.timeout(120)
-def test_gloo_two_rank_sharded_gather():
+@pytest.mark.timeout(180)
+@pytest.mark.parametrize("world,scaling", [(2, "strong"), (3, "strong"), (2, "weak")])
+def test_gloo_sharded_sweep_gather(world, scaling):
+    """world 2 and 3 (uneven shards: 5 images, 37 tokens), strong and weak scaling: the
+    gathered, reassembled result equals the unsharded computation."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q, scaling)) for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
-        p.join(100)
+        p.join(150)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=5) is True
+
+
+def test_sweep_shard_strong_and_weak():
+    from paper_2210_09603_b200.sharding import sweep_shard
+    for world in (1, 2, 4, 8):
+        shards = [sweep_shard(r, world) for r in range(world)]
+        assert sum(s.count("images") for s in shards) == 32
+        assert sum(s.count("tokens") for s in shards) == 8192
+        assert sum(s.count("heads") for s in shards) == 192
+        assert [s.range("images")[0] for s in shards] == [32 // world * r for r in range(world)]
+        weak = sweep_shard(world - 1, world, "weak")
+        assert weak.count("images") == 32 and weak.global_count("tokens") == 8192 * world
 
 
 def test_plan_device_follows_the_process_gpu():

@@ -90,13 +90,19 @@ def _ffn(t, cfg, seed=91):
     return got, (x, w1, b1, w2, b2)
 
 
-def _ffn_ok(got, args):
-    """bf16 H modelled: max_rel_error <= 2e-2 (SURVEY §8c chain tolerance); unmodelled,
-    relative to the output scale <= 1e-2 (tests/test_gpu_gemm.py::test_ffn_chain)."""
-    want_h = port.ffn(*args, round_h=port.round_bf16)
-    want = port.ffn(*args)
-    return (port.max_rel_error(got, want_h) <= 2e-2 and
-            np.abs(got - want).max() / np.abs(want).max() <= 1e-2)
+def _ffn_err(got, args):
+    """Chain error with the device's bf16 storage of H modelled: |got - ref| over
+    max(1, |ref|, rms(ref)) -- the scale-aware form of max_rel_error that the
+    tuner's gate uses.  At BERT widths O = H W2 sums 3072 terms of |H| ~ 10; where
+    they cancel, |O| is tiny and a per-element relative error only measures the
+    cancellation (round 1's element-wise gate rejected every split-K schedule for
+    that reason), so the floor is the output's rms."""
+    want = port.ffn(*args, round_h=port.round_bf16)
+    den = np.maximum(np.maximum(1.0, np.abs(want)), np.sqrt(np.mean(want ** 2)))
+    return float((np.abs(got - want) / den).max())
+
+
+FFN_TOL = 1e-2  # bf16 output (2^-9 relative) + tanh.approx GELU + bf16 H rounding flips
 
 
 def test_tuned_ffn_schedule_at_bert_dims():
@@ -105,7 +111,8 @@ def test_tuned_ffn_schedule_at_bert_dims():
     if key not in cache:
         pytest.skip("ffn not tuned")
     got, args = _ffn(128, ScheduleConfig(**cache[key]["config"]))
-    assert _ffn_ok(got, args)
+    err = _ffn_err(got, args)
+    assert err <= FFN_TOL, err
 
 
 @pytest.mark.parametrize("which", ["qk", "pv"])
@@ -137,8 +144,9 @@ def test_whole_space_ffn_chain():
     bad = []
     for i, cfg in enumerate(schedule_space("matmul")):
         got, args = _ffn(128, cfg, seed=95)
-        if not _ffn_ok(got, args):
-            bad.append((i, cfg))
+        err = _ffn_err(got, args)
+        if not err <= FFN_TOL:
+            bad.append((i, cfg.block_m, cfg.block_n, cfg.split_k, err))
     assert not bad, bad
 
 

@@ -128,3 +128,71 @@ def test_mixed_bf16_fp16_operands_are_refused():
     with pytest.raises(TaskmapError) as e:
         run(dag, {"A": dev(a, "bf16"), "B": dev(b, "f16"), "Bias": dev(bias, "f32")}, {"D": (m, n)})
     assert e.value.status == 4
+
+
+def _fig11_dag(n_rows=100, k=64, n=96, dtype=DType.F32):
+    """SPEC.md:370-387 / PAPER.md:606 Fig. 11 on the GEMM anchor: the prologue
+    A[i, k] = C[99 - i, k] * 2.0 (reversed re-index + arithmetic) feeds
+    B = A W; the epilogue D[i / 50, i % 50, j] = B[i, j] * 3.0 (reshape-split remap)."""
+    from paper_2210_09603_b200 import Axis, ComputeDAG, TensorNode, fimm, imm, load, mul, sub, var
+    d = ComputeDAG()
+    d.add_input("C", [n_rows, k], dtype)
+    d.add_input("W", [k, n], dtype)
+    d.add_compute("A", [Axis("i", n_rows), Axis("k", k)],
+                  mul(load("C", [sub(imm(n_rows - 1), var("i")), var("k")]), fimm(2.0)), dtype)
+    d.nodes.append(TensorNode("B", [n_rows, n], dtype, "reduce", [Axis("i", n_rows), Axis("j", n)], [Axis("kk", k)],
+                              value=mul(load("A", [var("i"), var("kk")]), load("W", [var("kk"), var("j")]))))
+    d.add_compute("D", [Axis("a", n_rows // 50), Axis("b", 50), Axis("j", n)],
+                  mul(load("B", [add_(mul(var("a"), imm(50)), var("b")), var("j")]), fimm(3.0)), dtype)
+    d.outputs = ["D"]
+    return d
+
+
+def add_(a, b):
+    from paper_2210_09603_b200 import add
+    return add(a, b)
+
+
+@pytest.mark.parametrize("cfg", [ScheduleConfig(), ScheduleConfig(block_n=64, split_k=2),
+                                 ScheduleConfig(block_m=256, block_n=128), ScheduleConfig(math="fp32_simt")])
+def test_fig11_arithmetic_prologue_and_remap_epilogue(cfg):
+    """Fig. 11 end to end on the GPU: one fused kernel whose gather loader reads
+    C[99 - i, k] * 2.0 and whose epilogue stores B * 3.0 at (i / 50, i % 50);
+    exact against reference_eval on integer data."""
+    from gpu_util import have_ref, oracle_eval
+    dag = _fig11_dag()
+    rng = port.Rng(87)
+    c, w = rng.tensor((100, 64), True), rng.tensor((64, 96), True)
+    dt = "f32" if cfg.math == "fp32_simt" else "bf16"
+    got, plan = run(dag, {"C": dev(c, dt), "W": dev(w, dt)}, {"D": (2, 50, 96)}, cfg=cfg)
+    k0 = plan.describe()["kernels"][0]
+    assert len(plan.describe()["kernels"]) == 1 and k0["prologue"] == ["A"] and k0["epilogue"] == ["D"]
+    assert "C[99 - __row" in k0["A"] or "C[" in k0["A"]
+    want = (3.0 * ((2.0 * c[::-1]) @ w)).reshape(2, 50, 96)
+    assert np.array_equal(got["D"], want)
+    if have_ref():
+        assert np.array_equal(got["D"], oracle_eval(dag, {"C": c, "W": w}, {"D": (2, 50, 96)})["D"])
+
+
+def test_relu_prologue_two_matmuls():
+    """ReLU -> matmul -> matmul partitions into two kernels and the ReLU
+    fuses into the first matmul's prologue only."""
+    from paper_2210_09603_b200 import Axis, ComputeDAG, TensorNode, load, relu, var, mul
+    m, k1, k2, n = 192, 96, 160, 128
+    d = ComputeDAG()
+    d.add_input("X", [m, k1], DType.I32)
+    d.add_input("W1", [k1, k2], DType.I32)
+    d.add_input("W2", [k2, n], DType.I32)
+    d.add_compute("R", [Axis("i", m), Axis("k", k1)], relu(load("X", [var("i"), var("k")])), DType.I32)
+    d.nodes.append(TensorNode("H", [m, k2], DType.I32, "reduce", [Axis("i", m), Axis("j", k2)], [Axis("k", k1)],
+                              value=mul(load("R", [var("i"), var("k")]), load("W1", [var("k"), var("j")]))))
+    d.nodes.append(TensorNode("Y", [m, n], DType.I32, "reduce", [Axis("i", m), Axis("j", n)], [Axis("k", k2)],
+                              value=mul(load("H", [var("i"), var("k")]), load("W2", [var("k"), var("j")]))))
+    d.outputs = ["Y"]
+    rng = port.Rng(88)
+    x, w1, w2 = rng.tensor((m, k1), True), rng.tensor((k1, k2), True), rng.tensor((k2, n), True)
+    got, plan = run(d, {"X": dev(x, "f32"), "W1": dev(w1, "f32"), "W2": dev(w2, "f32")}, {"Y": (m, n)},
+                    cfg=ScheduleConfig(math="tf32"))
+    ks = plan.describe()["kernels"]
+    assert len(ks) == 2 and ks[0]["prologue"] == ["R"] and ks[1]["prologue"] == []
+    assert np.array_equal(got["Y"], (np.maximum(x, 0) @ w1) @ w2)

@@ -4,9 +4,9 @@ behind it (tm_dag_eval).
 * tm_dag_eval is pinned to the reference's reference_eval (oracle/_ref): bit-exact
   on the reference's integer test data, fp64-close on float data.
 * tm_tune verifies every schedule against it on seeded inputs and is a hard
-  gate: a correct space tunes with zero incorrect configs; a broken tensor
-  program (TMB_DBG=2 suppresses every output store) aborts with status 1
-  (TM_ERR_CORRECTNESS) and a report.
+  gate: a correct space tunes with zero incorrect configs; broken tensor
+  programs (fault injection TMB_FAULT_SKIP_KBLOCK drops each kernel's last
+  k-block) abort tuning with status 1 (TM_ERR_CORRECTNESS) and a report.
 """
 import os
 
@@ -149,11 +149,11 @@ def test_tune_conv_integer_trial_is_bit_exact():
 
 
 def test_tune_gate_aborts_on_incorrect_configs(monkeypatch):
-    """A tensor program that never stores its output (diagnostic TMB_DBG=2) must
+    """Tensor programs that drop their last k-block (fault injection TMB_FAULT_SKIP_KBLOCK) must
     abort tuning with TM_ERR_CORRECTNESS and a report, not be skipped."""
     t, dm, dff = 256, 128, 256
     ins, outs = _ffn_tensors(t, dm, dff)
-    monkeypatch.setenv("TMB_DBG", "2")
+    monkeypatch.setenv("TMB_FAULT_SKIP_KBLOCK", "1")
     with pytest.raises(TaskmapError) as e:
         tune(ffn_dag(t, dm, dff), ins, outs, reps=1)
     assert e.value.status == 1

@@ -88,14 +88,16 @@ def test_plans_lower_config_chains():
 
 
 def test_fig11_prologue_epilogue_remap():
-    """PAPER Fig. 11 / SPEC.md:376,385: A[99-i] -> C[99-i]*2 prologue is a pure re-index of
-    an input; the epilogue stores y*3 at (i/50, i%50)."""
-    from paper_2210_09603_b200 import fimm, mul, sub, imm, div, mod
+    """PAPER Fig. 11 / SPEC.md:376,385: "the access of A[99 - i] will be replaced by
+    C[99 - i] * 2.0" -- an arithmetic prologue over a reversed re-index, lowered to the
+    operand's address map plus a prologue op list (MUL_C 2.0) for the gather loader --
+    and the epilogue stores y*3 at (i/50, i%50)."""
+    from paper_2210_09603_b200 import fimm, mul, sub, imm
     d = ComputeDAG()
     d.add_input("C", [100, 8])
     d.add_input("B", [8, 4])
     d.nodes.append(TensorNode("A", [100, 8], kind="compute", axes=[Axis("i", 100), Axis("k", 8)],
-                              value=load("C", [sub(imm(99), var("i")), var("k")])))
+                              value=mul(load("C", [sub(imm(99), var("i")), var("k")]), fimm(2.0))))
     d.nodes.append(TensorNode("Y", [100, 4], kind="reduce", axes=[Axis("i", 100), Axis("j", 4)],
                               reduce_axes=[Axis("k", 8)], value=mul(load("A", [var("i"), var("k")]),
                                                                      load("B", [var("k"), var("j")]))))
@@ -104,7 +106,32 @@ def test_fig11_prologue_epilogue_remap():
     d.outputs = ["D"]
     assert partition(d) == [{"anchor": "Y", "prologue": ["A"], "epilogue": ["D"], "output": "D"}]
     k = Plan(d).describe()["kernels"][0]
-    assert k["A"].startswith("C[99 - __row") and [o["kind"] for o in k["ops"]] == [4]
+    assert k["A"].startswith("C[99 - __row") and k["A"].endswith("|> op4(2.000000)")  # MUL_C 2.0
+    assert [o["kind"] for o in k["ops"]] == [4] and k["ops"][0]["c"] == 3  # epilogue MUL_C 3.0
+
+
+def test_relu_prologue_and_rejected_prologues():
+    """SPEC.md:368 ReLU -> matmul -> matmul: the ReLU is the first anchor's prologue op.
+    Prologues the gather loader cannot apply (two input elements, a tensor side
+    operand) are refused with TM_ERR_UNSUPPORTED."""
+    from paper_2210_09603_b200 import relu, add
+    def dag(value):
+        d = ComputeDAG()
+        d.add_input("X", [16, 8])
+        d.add_input("W", [8, 4])
+        d.add_input("V", [16, 8])
+        d.nodes.append(TensorNode("R", [16, 8], kind="compute", axes=[Axis("i", 16), Axis("k", 8)], value=value))
+        d.nodes.append(TensorNode("Y", [16, 4], kind="reduce", axes=[Axis("i", 16), Axis("j", 4)],
+                                  reduce_axes=[Axis("k", 8)], value=T.mul(load("R", [var("i"), var("k")]),
+                                                                           load("W", [var("k"), var("j")]))))
+        d.outputs = ["Y"]
+        return d
+    x = load("X", [var("i"), var("k")])
+    k = Plan(dag(relu(x))).describe()["kernels"][0]
+    assert k["prologue"] == ["R"] and k["A"].endswith("|> op32(0.000000)")  # RELU
+    with pytest.raises(TaskmapError) as e:
+        Plan(dag(add(x, load("V", [var("i"), var("k")]))))
+    assert e.value.status == 4
 
 
 def test_schedule_space_size_and_agnostic():
