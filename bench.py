@@ -122,10 +122,11 @@ def build_sweep(torch, device, shard, tuner=None, tune_mode="auto", log=None):
         return t.contiguous(memory_format=torch.channels_last) if cl else t
 
     def conv_input(L, B):
-        if L.c < 8:  # 16-byte padded channels-last (NHWC8): the TMA-able layout for C < 8
-            xb = torch.zeros((B, L.h, L.h, 8), device=device, dtype=torch.bfloat16)
+        if L.c < 8:  # channels-last with pixels padded to 4 (C <= 4: 8-byte pixels, the row-band
+            cp = 4 if L.c <= 4 else 8  # kernel's layout for stride 2) or 8 channels (16-byte pixels)
+            xb = torch.zeros((B, L.h, L.h, cp), device=device, dtype=torch.bfloat16)
             xb[..., :L.c] = rnd((B, L.h, L.h, L.c))
-            return xb.as_strided((B, L.c, L.h, L.h), (L.h * L.h * 8, 1, L.h * 8, 8))
+            return xb.as_strided((B, L.c, L.h, L.h), (L.h * L.h * cp, 1, L.h * cp, cp))
         return rnd((B, L.c, L.h, L.h), cl=True)
 
     def pick(key, dag, ins, outs, default):

@@ -50,6 +50,7 @@ struct EpiOp {
   Addr a;
 };
 
+constexpr int kMaxSmem = 232448;  // 227 KB opt-in dynamic shared memory per CTA on sm_100
 constexpr int kMaxEpiOps = 8;
 constexpr int kMaxMatOps = 2;
 constexpr int kTraceTiles = 64;
@@ -65,6 +66,10 @@ constexpr int kTraceEvents = 16;  // 0-7 role events (TraceEv); tile 0: 14/15 = 
 constexpr int out_stage_row_bytes(int bn, int cg) {
   return ((bn == 256 && cg == 1) || bn == 64 || bn == 96 || bn == 192) ? 64 : 128;
 }
+// Row-band conv kernel (conv_rowband.cuh) output staging: 128-byte (64-column)
+// swizzled row segments, one TMA store per warp per 64 columns (its epilogue
+// groups alternate whole tiles instead of splitting columns).
+constexpr int kRbOutRow = 128;
 // trace events per tile
 enum TraceEv : int32_t {
   TR_PROD_FIRST = 0,  // producer: first k-block slot acquired
@@ -87,9 +92,11 @@ enum LoaderKind : int32_t {
   LD_IM2COL_TMA8 = 6,   // small-C conv (C <= 8, 16-byte padded channels-last X): one
                         // TMA im2col box {8 ch x 128 px} per tap, 8 taps per k-block,
                         // no-swizzle K-major smem layout; K order (tap, c < 8)
-  LD_IM2COL_G8 = 7      // same layout and K order as LD_IM2COL_TMA8, gathered by the
+  LD_IM2COL_G8 = 7,     // same layout and K order as LD_IM2COL_TMA8, gathered by the
                         // 128 loader threads: one 16-byte load per (pixel, tap), the
                         // channels >= C masked to zero (no per-box TMA cost: 49 taps)
+  LD_ROWBAND = 8        // no im2col tile at all: staged input rows read by the MMA through
+                        // overlapping no-swizzle descriptors (tm_rowband_kernel)
 };
 
 // An elementwise prologue op applied to every operand element the gather
@@ -182,6 +189,24 @@ struct GemmParams {
   // lean drain writes bf16 rows straight from registers (16-byte stores) instead
   // of smem staging + TMA store: row-major output, 16-byte aligned rows, N % 8 == 0
   int32_t out_direct;
+  // Row-band implicit GEMM (tm_rowband_kernel, conv_rowband.cuh): small-C convs
+  // whose input pixels are padded to cpad channels with stride * cpad == 8, so
+  // consecutive output pixels' windows start 16 bytes apart in a staged input row
+  // and every tcgen05.mma reads its A operand straight out of the staged rows.
+  int32_t rb_T;        // output rows per band
+  int32_t rb_rows;     // staged input rows per TMA box (4 boxes per band >= stride * (T - 1) + kh rows)
+  int32_t rb_rowb;     // bytes per staged input row (whole 16- or 128-byte chunks)
+  int32_t rb_off0;     // byte offset of output pixel 0's window inside a staged row
+  int32_t rb_T0;       // output rows of a CTA's first band (short: the MMA starts sooner)
+  int32_t rb_rows0;    // staged input rows per box of the first band
+  int32_t rb_steps;    // K16 MMA steps per filter row (= 8 * cpad / 16)
+  int32_t rb_g0;       // chunk coordinate of a staged row's first chunk (<= 0: left padding)
+  int32_t rb_total;    // output rows N * Ho
+  int32_t rb_cpad;     // channels per staged pixel
+  int32_t rb_fix;      // zero channels [C, cpad) of every staged pixel (padding lanes)
+  int32_t rb_bbytes;   // bytes of the packed filter image
+  int32_t rb_pad3_;
+  const void* rb_bimg; // packed filter smem image [kh][steps][F/8][2][8 rows][16 B]
   int32_t n_ops;
   int32_t has_mat;  // any SIDE_MAT op
   int32_t out_dtype;

@@ -71,7 +71,6 @@ struct GemmCfg {
   static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128 must be 16..256 step 16");
 };
 
-constexpr int kMaxSmem = 232448;  // 227 KB opt-in dynamic shared memory per CTA on sm_100
 
 // deepest ring (<= 8 stages) that fits next to the epilogue buffers
 constexpr int stages_for(int bn, int cg, bool generic = true) {

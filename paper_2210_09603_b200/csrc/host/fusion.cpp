@@ -783,6 +783,116 @@ bool tma_ok_mnmajor(const Fit& f, const tm_tensor& t, int64_t rows, int64_t k, i
   if ((f.c1 * es) % 16 || (f.c2 * es) % 16) return false;
   return (reinterpret_cast<uintptr_t>(t.data) + f.off * es) % 16 == 0;
 }
+
+// Row-band implicit GEMM (conv_rowband.cuh) for a conv anchor whose input
+// pixels are padded to cpad in {4, 8} channels (C <= cpad) with stride * cpad
+// == 8, Wo <= 128, kw + shift <= 8, and a canonical epilogue storing bf16/fp16
+// channels-last rows without a residual.  Called once the generic operand /
+// epilogue binding is known; returns false (leaving k untouched) otherwise.
+bool bind_rowband(const SubgraphPlan& sp, const std::map<std::string, tm_tensor>& env, BoundKernel& k, Exec& ex,
+                  int want_dt, int sms) {
+  GemmParams& p = k.p;
+  if (std::getenv("TMB_NO_ROWBAND")) return false;
+  if (sp.a.kind != OperandPlan::Im2col || sp.b.kind != OperandPlan::ConvFilter || k.simt || k.tf32) return false;
+  if (!p.canon || p.canon_res_op >= 0 || !p.out_tma || p.out_dtype != want_dt || sp.batch != 1) return false;
+  const ConvInfo& c = sp.a.conv;
+  const tm_tensor& x = lookup(env, c.x_tensor);
+  const tm_tensor& w = lookup(env, sp.b.conv.w_tensor);
+  const int64_t cpad = x.stride[3];
+  if (x.dtype != want_dt || x.stride[1] != 1 || (cpad != 4 && cpad != 8) || c.c > cpad || c.stride * cpad != 8) return false;
+  if ((c.w * cpad) % 8 || x.stride[2] < c.w * cpad || x.stride[2] % 8 || x.stride[0] < c.h * x.stride[2] ||
+      x.stride[0] % 8 || reinterpret_cast<uintptr_t>(x.data) % 16)
+    return false;
+  const int ppg = static_cast<int>(8 / cpad);  // pixels per 16-byte granule
+  const int shift = static_cast<int>((ppg - c.pad % ppg) % ppg);
+  const int64_t F = sp.N;  // output channels (the filter's rows)
+  if (c.wo > 128 || c.kw + shift > 8 || F > 256 || c.ho < 1) return false;
+  // output: rows = pixels (n, oh, ow) at stride lo, uniform across rows of pixels
+  const Addr& oa = p.out_a;
+  if (oa.s_col != 1 || oa.P < sp.M || oa.s_lo <= 0) return false;
+  const int es = 2;
+  const int bn = F <= 64 ? 64 : F <= 128 ? 128 : 256;
+  const int steps = static_cast<int>(cpad / 2);  // 8 taps * cpad channels * 2 B / 32 B per K16 step
+  // staged rows are loaded in 128-byte chunks when an image row is a whole
+  // number of them (a TMA box with 128-byte inner rows moves ~8x fewer lines
+  // than one with 16-byte granules), else in 16-byte granules; the left
+  // padding (pad + shift pixels) is rounded up to whole chunks of zero fill
+  const int64_t row_bytes = c.w * cpad * 2;
+  const int chunk = row_bytes % 128 == 0 ? 128 : 16;
+  const int64_t lp_bytes = ((c.pad + shift) * cpad * 2 + chunk - 1) / chunk * chunk;  // left zero fill
+  const int off0 = static_cast<int>(lp_bytes - (c.pad + shift) * cpad * 2);  // window of ow = 0
+  // (rows are whole 128-byte units: each TMA box lands 128-byte aligned)
+  const int rowb = static_cast<int>((off0 + 16 * 127 + 16 * cpad + 127) / 128 * 128);
+  const int bbytes = static_cast<int>(c.kh * steps * bn * 32);
+  int T = 0;
+  const int tmax = std::getenv("TMB_RB_T") ? std::max(1, std::atoi(std::getenv("TMB_RB_T"))) : 16;  // diagnostics
+  constexpr int kBoxes = 4;  // conv_rowband.cuh kRbLoadWarps
+  auto rbox_of = [&](int t) { return static_cast<int>((c.stride * (t - 1) + c.kh + kBoxes - 1) / kBoxes); };
+  for (int t = tmax; t >= 1 && !T; --t)
+    if (rowband_smem(kBoxes * rbox_of(t), rowb, bbytes, bn) <= kMaxSmem) T = t;
+  if (!T) return false;
+  // filter image, packed once at bind (an inference constant of the bound plan)
+  ConvGeom& g = p.conv;
+  g.n = static_cast<int32_t>(c.n); g.c = static_cast<int32_t>(c.c); g.h = static_cast<int32_t>(c.h);
+  g.w = static_cast<int32_t>(c.w); g.f = static_cast<int32_t>(F); g.kh = static_cast<int32_t>(c.kh);
+  g.kw = static_cast<int32_t>(c.kw); g.stride = static_cast<int32_t>(c.stride); g.pad = static_cast<int32_t>(c.pad);
+  g.ho = static_cast<int32_t>(c.ho); g.wo = static_cast<int32_t>(c.wo);
+  g.x = x.data; g.x_dtype = x.dtype; g.wt = w.data; g.w_dtype = w.dtype;
+  for (int d = 0; d < 4; ++d) { g.sx[d] = x.stride[d]; g.sw[d] = w.stride[d]; }
+  void* img = nullptr;
+  if (cudaMalloc(&img, bbytes) != cudaSuccess) fail_cuda("cudaMalloc failed for the row-band filter image");
+  ex.scratch.push_back(img);
+  pack_rowband_filter(g, static_cast<int>(cpad), shift, steps, bn, img, want_dt);
+  // staged-row view {chunk elements, chunks per row, H, N} (no swizzle); the
+  // first band's box (tma_b slot) has fewer rows
+  const int T0 = std::min(T, 4);
+  for (int which = 0; which < 2; ++which) {
+    const uint64_t dims[4] = {(uint64_t)(chunk / es), (uint64_t)(row_bytes / chunk), (uint64_t)c.h, (uint64_t)c.n};
+    const uint64_t strides[3] = {(uint64_t)chunk, (uint64_t)x.stride[2] * es, (uint64_t)x.stride[0] * es};
+    const int t = which == 0 ? T : T0;
+    const uint32_t box[4] = {(uint32_t)(chunk / es), (uint32_t)(rowb / chunk), (uint32_t)rbox_of(t), 1u};
+    make_tma_2d3d(which == 0 ? k.tma_a : k.tma_b, x.data, x.dtype, 4, dims, strides, box, 0);
+  }
+  // output view {F, Wo, N*Ho}: one tile = one output row, lanes >= Wo clipped
+  {
+    const uintptr_t base = reinterpret_cast<uintptr_t>(p.out) + oa.offset * es;
+    const uint64_t dims[3] = {(uint64_t)F, (uint64_t)c.wo, (uint64_t)(c.n * c.ho)};
+    const uint64_t strides[2] = {(uint64_t)(oa.s_lo * es), (uint64_t)(oa.s_lo * c.wo * es)};
+    const uint32_t box[3] = {static_cast<uint32_t>(kRbOutRow / es), 32u, 1u};
+    make_tma_2d3d(k.tma_c, reinterpret_cast<const void*>(base), p.out_dtype, 3, dims, strides, box, kRbOutRow);
+  }
+  p.rb_T = T;
+  p.rb_rows = rbox_of(T);
+  p.rb_rowb = rowb;
+  p.rb_off0 = off0;
+  p.rb_T0 = T0;
+  p.rb_rows0 = rbox_of(T0);
+  p.rb_steps = steps;
+  p.rb_g0 = static_cast<int32_t>(-lp_bytes / chunk);
+  p.rb_total = static_cast<int32_t>(c.n * c.ho);
+  p.rb_cpad = static_cast<int32_t>(cpad);
+  p.rb_fix = (c.c < cpad && !std::getenv("TMB_RB_NOFIX")) ? 1 : 0;  // NOFIX: diagnostics only
+  if (const char* d = std::getenv("TMB_DBG")) p.dbg = std::atoi(d);  // 11-13: MMA operand-layout timing probes
+  p.rb_bbytes = bbytes;
+  p.rb_bimg = img;
+  k.rowband = 1;
+  p.a_loader = LD_ROWBAND;
+  p.b_loader = LD_TMA_K;
+  k.bn = bn;
+  k.cg = 1;
+  k.smem = rowband_smem(kBoxes * p.rb_rows, rowb, bbytes, bn);
+  k.grid = static_cast<int>(std::min<int64_t>(sms, c.n * c.ho));
+  p.split_k = 1;
+  if (std::getenv("TMB_TRACE")) {  // per-tile role timeline (tm_exec_trace)
+    void* tr = nullptr;
+    const size_t tb = size_t(k.grid) * kTraceTiles * kTraceEvents * 8;
+    if (cudaMalloc(&tr, tb) != cudaSuccess || cudaMemset(tr, 0, tb) != cudaSuccess)
+      fail_cuda("cudaMalloc failed for the trace buffer");
+    ex.scratch.push_back(tr);
+    p.trace = static_cast<long long*>(tr);
+  }
+  return true;
+}
 }  // namespace
 
 int intermediate_dtype(const tm_tensor* inputs, int n_in) {
@@ -1143,8 +1253,12 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
                            : 0;
       }
     }
-    if (const char* sw = std::getenv("TMB_MN_SWAP")) p.mn_lbo_sbo_swap = std::atoi(sw);
     p.fast_math = p.out_dtype != TM_F32;  // approximate tanh only where the output rounding dominates
+    if (bind_rowband(sp, env, k, *ex, want_dt, sms)) {
+      ex->kernels.push_back(k);
+      continue;
+    }
+    if (const char* sw = std::getenv("TMB_MN_SWAP")) p.mn_lbo_sbo_swap = std::atoi(sw);
     // fault injection for the tuner-gate test (tests/test_gpu_tuner.py): every kernel
     // silently drops its last k-block, so every schedule computes a wrong result
     if (std::getenv("TMB_FAULT_SKIP_KBLOCK") && p.num_kb > 1) {

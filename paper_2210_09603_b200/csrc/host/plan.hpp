@@ -78,6 +78,8 @@ struct BoundKernel {
   GemmParams p;
   int bn = 128, stages = 4, tf32 = 0, grid = 148, simt = 0, cg = 1;
   int generic = 1;  // 0: compact instantiation (TMA loaders + canonical epilogue only)
+  int rowband = 0;  // 1: tm_rowband_kernel (conv_rowband.cuh); tma_a = staged-row map, smem = its layout
+  int smem = 0;
   alignas(64) unsigned char tma_a[128];
   alignas(64) unsigned char tma_b[128];
   alignas(64) unsigned char tma_c[128];  // output map (row-major outputs, TMA-store epilogue)
@@ -97,6 +99,9 @@ int num_sms(int device);
 void launch_bound(const BoundKernel& k, void* stream);
 int kernel_stages(const BoundKernel& k);  // ring depth of the instantiation launch_bound will pick
 void pack_filter(const ConvGeom& g, int kp, void* out, int out_dtype);  // bf16/fp16 [f][kp] in the GEMM K order
+// filter image of the row-band kernel: [kh][steps][bn/8][2][8][8] 16-bit, K order (fw + shift, c < cpad)
+void pack_rowband_filter(const ConvGeom& g, int cpad, int shift, int steps, int bn, void* out, int out_dtype);
+int rowband_smem(int rows, int rowb, int bbytes, int bn);
 // storage dtype of materialised intermediates for these inputs: f32 if any input
 // is f32, fp16 if the 16-bit inputs are all fp16, else bf16
 int intermediate_dtype(const tm_tensor* inputs, int n_in);

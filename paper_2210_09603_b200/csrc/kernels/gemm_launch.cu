@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <cstring>
+#include <string>
 #include <mutex>
 #include <type_traits>
 
@@ -64,12 +65,22 @@ void make_tma_2d3d(void* map, const void* ptr, int dtype, int rank, const uint64
     e[i] = 1;
   }
   for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
-  check_cu(enc(reinterpret_cast<CUtensorMap*>(map), tma_dtype(dtype), rank, const_cast<void*>(ptr), d, s, b,
-               e, CU_TENSOR_MAP_INTERLEAVE_NONE,
-               swizzle == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
-                              : (swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE),
-               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE),
-           "cuTensorMapEncodeTiled");
+  const CUresult r = enc(reinterpret_cast<CUtensorMap*>(map), tma_dtype(dtype), rank, const_cast<void*>(ptr), d, s, b,
+                         e, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                         swizzle == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                        : (swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE),
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    std::string dims_s, str_s, box_s;
+    for (int i = 0; i < rank; ++i) {
+      dims_s += std::to_string(dims[i]) + " ";
+      box_s += std::to_string(box[i]) + " ";
+      if (i < rank - 1) str_s += std::to_string(strides_bytes[i]) + " ";
+    }
+    taskmap::fail_cuda("cuTensorMapEncodeTiled failed with CUresult ", static_cast<int>(r), " (rank ", rank, ", dims ",
+                       dims_s, ", strides ", str_s, ", box ", box_s, ", swizzle ", swizzle, ", address ",
+                       reinterpret_cast<uintptr_t>(ptr) % 128, " mod 128)");
+  }
 }
 
 void make_tma_im2col(void* map, const void* ptr, int dtype, const uint64_t* dims_cwhn,
@@ -205,7 +216,8 @@ void launch_bound(const BoundKernel& k, void* stream) {
   if (k.simt) {
     launch_simt(k, stream);
     ok = true;
-  } else if (k.cg == 2) ok = launch_cg2(k, s);
+  } else if (k.rowband) ok = launch_rowband(k, s);
+  else if (k.cg == 2) ok = launch_cg2(k, s);
   else if (k.tf32) ok = launch_cg1_generic_tf32(k, s);
   else if (!k.generic) ok = launch_cg1_fast(k, s);
   else ok = launch_cg1_generic_bf16(k, s);

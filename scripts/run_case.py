@@ -63,10 +63,11 @@ def main():
         B = W.RESNET_BATCH
         cl = not a.nchw
         fmt = torch.channels_last if cl else torch.contiguous_format
-        if L.c < 8 and cl:  # 16-byte padded channels-last (NHWC8) view, TMA-able
-            xb = torch.zeros((B, L.h, L.h, 8), device=dev, dtype=torch.bfloat16)
+        if L.c < 8 and cl:  # padded channels-last view (NHWC4 for C <= 4, else NHWC8), as bench.py
+            cp = 4 if L.c <= 4 else 8
+            xb = torch.zeros((B, L.h, L.h, cp), device=dev, dtype=torch.bfloat16)
             xb[..., :L.c] = rnd((B, L.h, L.h, L.c))
-            x0 = xb.as_strided((B, L.c, L.h, L.h), (L.h * L.h * 8, 1, L.h * 8, 8))
+            x0 = xb.as_strided((B, L.c, L.h, L.h), (L.h * L.h * cp, 1, L.h * cp, cp))
         else:
             x0 = rnd((B, L.c, L.h, L.h)).contiguous(memory_format=fmt)
         ins = [x0,
@@ -146,6 +147,7 @@ def main():
         print(f"CTA span cycles: min {span.min()} median {np.median(span):.0f} max {span.max()}; "
               f"per-tile MMA issue span mean {mma[mma > 0].mean():.0f}; epilogue mean {epi[epi > 0].mean():.0f}")
     print(json.dumps({"case": a.case, "ms": ms, "tflops": flops / ms / 1e9, "launches": ex.num_launches,
+                      "kernel": ex.kernel_info(0),
                       "plan": plan.describe()["kernels"][0]["A"] + " x " + plan.describe()["kernels"][0]["B"]}))
 
 

@@ -3,7 +3,7 @@
 For every workload key of tuning_cache.json (the configs bench.py binds), the
 cached ScheduleConfig is bound on that workload's real geometry at a reduced
 batch -- ResNet-50 convs with their true C/H/F/k/s/p at 1-2 images in the bench's
-channels-last layout (NHWC8 for conv1), the BERT FFN at 768/3072 on 128 tokens,
+channels-last layout (NHWC4 for conv1), the BERT FFN at 768/3072 on 128 tokens,
 attention at 128 x 64 on 4 heads -- and compared with the oracle port (pinned to
 reference_eval by tests/golden): exact on the reference's integer test data
 (bf16 outputs: equal to round_bf16 of the exact result), toleranced on floats.
@@ -38,17 +38,18 @@ def _bf16(a):
 
 
 def _conv_case(L, n, cfg, seed):
-    """bench.build_sweep's layouts: channels-last X (NHWC8 for C < 8) and W, fp32
+    """bench.build_sweep's layouts: channels-last X (NHWC4 for C <= 4, NHWC8 for C < 8) and W, fp32
     BN scale/shift, channels-last bf16 output."""
     torch = _torch()
     rng = port.Rng(seed)
     x = rng.tensor((n, L.c, L.h, L.h), True)
     wt = rng.tensor((L.f, L.c, L.k, L.k), True)
     scale, shift = rng.tensor((L.f,), True), rng.tensor((L.f,), True)
-    if L.c < 8:
-        xb = torch.zeros((n, L.h, L.h, 8), dtype=torch.bfloat16, device="cuda")
+    if L.c < 8:  # pixels padded to 4 (C <= 4) or 8 channels, as bench.py stores them
+        cp = 4 if L.c <= 4 else 8
+        xb = torch.zeros((n, L.h, L.h, cp), dtype=torch.bfloat16, device="cuda")
         xb[..., :L.c] = _bf16(x).permute(0, 2, 3, 1)
-        xd = xb.as_strided((n, L.c, L.h, L.h), (L.h * L.h * 8, 1, L.h * 8, 8))
+        xd = xb.as_strided((n, L.c, L.h, L.h), (L.h * L.h * cp, 1, L.h * cp, cp))
     else:
         xd = _bf16(x).contiguous(memory_format=torch.channels_last)
     wd = _bf16(wt).contiguous(memory_format=torch.channels_last)
