@@ -100,7 +100,7 @@ class ClockSampler:
 # ---------------------------------------------------------------- workload --
 def cfg_str(cfg):
     return f"bm{cfg.block_m}/bn{cfg.block_n}/sk{cfg.split_k}/{'deep' if cfg.pipeline else 'db'}/r{cfg.raster}" + \
-        (f"/g{cfg.grid}" if cfg.grid else "")
+        (f"/g{cfg.grid}" if cfg.grid else "") + (f"/bk{cfg.block_k}" if cfg.math == "fp32_simt" else "")
 
 
 def build_sweep(torch, device, shard, tuner=None, tune_mode="auto", log=None):
@@ -298,7 +298,8 @@ def config1_lines(torch, device, peak_tf, sm_mhz, reps=50):
         a, b, bias = r(m, k, dt=dt), r(k, n, dt=dt), r(n)
         d = torch.empty((m, n), device=device, dtype=torch.float32)
         best = None
-        for cfg in ([ScheduleConfig(math=math)] if math == "fp32_simt" else
+        for cfg in ([ScheduleConfig(math=math, block_n=bn, block_k=bk) for bn in (128, 64) for bk in (8, 16)]
+                    if math == "fp32_simt" else
                     [ScheduleConfig(math=math, block_n=bn, split_k=sk) for bn in (128, 256) for sk in (1, 2, 4)]):
             ex = Plan(W.matmul_bias_relu_dag(m, n, k), cfg).bind([a, b, bias], [d])
             gr = Graph([ex] * reps)

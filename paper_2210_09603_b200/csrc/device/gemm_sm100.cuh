@@ -862,6 +862,10 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
   using Cfg = GemmCfg<BN, STAGES, TF32, CG, GENERIC>;
   constexpr int BK = Cfg::BK;
   constexpr int kTileM = kBM * CG;  // rows per tile (both CTAs of a pair)
+  // MN-major B: one 128-byte swizzle row holds MNB elements along N (64 bf16 / 32
+  // tf32); a block of MNB columns x BK k-rows occupies BK * 128 bytes of the slot
+  constexpr int MNB = kRowBytes / Cfg::kElem;
+  constexpr int MN_BLOCK_BYTES = BK * kRowBytes;
   const uint32_t rank = CG == 2 ? ptx::cluster_ctarank() : 0u;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((ptx::smem_u32(smem_raw) & 1023u) != 0u) __trap();  // SWIZZLE_128B tiles need 1 KB alignment
@@ -1025,11 +1029,11 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
                     ptx::tma_load_3d_2sm(b_tile, &tmB, lead_full, k0, n0, b);
                   } else {
                     if (p.b_mn4d) {
-                      ptx::tma_load_4d_2sm(b_tile, &tmB, lead_full, 0, k0, n0 / 64, b);
+                      ptx::tma_load_4d_2sm(b_tile, &tmB, lead_full, 0, k0, n0 / MNB, b);
                     } else {
 #pragma unroll 1
-                      for (int j = 0; j < BN / CG / 64; ++j)
-                        ptx::tma_load_3d_2sm(b_tile + j * (64 * kRowBytes), &tmB, lead_full, n0 + 64 * j, k0, b);
+                      for (int j = 0; j < BN / CG / MNB; ++j)
+                        ptx::tma_load_3d_2sm(b_tile + j * MN_BLOCK_BYTES, &tmB, lead_full, n0 + MNB * j, k0, b);
                     }
                   }
                 }
@@ -1075,11 +1079,11 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
                     ptx::tma_load_3d(b_tile, &tmB, &full[stage], k0, n0, b);
                   } else {
                     if (p.b_mn4d) {
-                      ptx::tma_load_4d(b_tile, &tmB, &full[stage], 0, k0, n0 / 64, b);
+                      ptx::tma_load_4d(b_tile, &tmB, &full[stage], 0, k0, n0 / MNB, b);
                     } else {
 #pragma unroll 1
-                      for (int j = 0; j < BN / 64; ++j)
-                        ptx::tma_load_3d(b_tile + j * (64 * kRowBytes), &tmB, &full[stage], n0 + 64 * j, k0, b);
+                      for (int j = 0; j < BN / MNB; ++j)
+                        ptx::tma_load_3d(b_tile + j * MN_BLOCK_BYTES, &tmB, &full[stage], n0 + MNB * j, k0, b);
                     }
                   }
                 }
@@ -1138,11 +1142,11 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
               ptx::tma_load_3d(b_tile, &tmB, &full[stage], k0, n0, b);
             } else if (p.b_loader == LD_TMA_MN) {
               if (p.b_mn4d) {
-                ptx::tma_load_4d(b_tile, &tmB, &full[stage], 0, k0, n0 / 64, b);
+                ptx::tma_load_4d(b_tile, &tmB, &full[stage], 0, k0, n0 / MNB, b);
               } else {
 #pragma unroll 1
-                for (int j = 0; j < BN / 64; ++j)
-                  ptx::tma_load_3d(b_tile + j * (64 * kRowBytes), &tmB, &full[stage], n0 + 64 * j,
+                for (int j = 0; j < BN / MNB; ++j)
+                  ptx::tma_load_3d(b_tile + j * MN_BLOCK_BYTES, &tmB, &full[stage], n0 + MNB * j,
                                    k0, b);
               }
             }
@@ -1617,8 +1621,8 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
       const bool a_g8 = p.a_loader == LD_IM2COL_G8;
       // operand format: tf32 (kind::tf32) / fp16 (0) or bf16 (1) for kind::f16
       const uint32_t idesc = ptx::make_idesc(kTileM, BN, TF32 ? 2u : (p.ab_f16 ? 0u : 1u), false, b_mn);
-      const uint32_t mn_lbo = p.mn_lbo_sbo_swap ? 1024u : 64u * kRowBytes;
-      const uint32_t mn_sbo = p.mn_lbo_sbo_swap ? 64u * kRowBytes : 1024u;
+      const uint32_t mn_lbo = p.mn_lbo_sbo_swap ? 1024u : static_cast<uint32_t>(MN_BLOCK_BYTES);
+      const uint32_t mn_sbo = p.mn_lbo_sbo_swap ? static_cast<uint32_t>(MN_BLOCK_BYTES) : 1024u;
       const uint32_t a0 = ptx::smem_u32(smA), b0 = ptx::smem_u32(smB);
       // 2 taps (2 x 16 B chunks of 2 KB boxes) per K16 for the C<=8 im2col layout
       // G8: taps adjacent (LBO 128 B along K, SBO 1024 B per 8 rows), 2 taps per K16

@@ -775,8 +775,8 @@ bool tma_ok_kmajor(const Fit& f, const tm_tensor& t, int64_t rows, int want_dt, 
   return base % 16 == 0;
 }
 
-bool tma_ok_mnmajor(const Fit& f, const tm_tensor& t, int64_t rows, int64_t k, int64_t batch) {
-  if (t.dtype != TM_BF16 && t.dtype != TM_F16) return false;
+bool tma_ok_mnmajor(const Fit& f, const tm_tensor& t, int64_t rows, int64_t k, int64_t batch, int want_dt) {
+  if (t.dtype != want_dt) return false;
   const int es = esize(t.dtype);
   if (f.lo != 1 || f.P < rows || f.c1 <= 0) return false;
   if (!batch_ok(f.c2, f.c1 * k, batch)) return false;
@@ -1109,23 +1109,29 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
                                      (uint64_t)(std::max<int64_t>(f.c2, f.lo * sp.N) * esize(opb->dtype))};
         const uint32_t box[3] = {(uint32_t)BK, (uint32_t)bn_cta, 1u};
         make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * esize(opb->dtype), opb->dtype, 3, dims, strides, box);
-      } else if (!k.tf32 && sp.b.pre.empty() && bn_cta % 64 == 0 && tma_ok_mnmajor(f, *opb, sp.N, sp.K, sp.batch)) {
+      } else if (!k.tf32 && sp.b.pre.empty() && bn_cta % (128 / esize(want_dt)) == 0 &&
+                 tma_ok_mnmajor(f, *opb, sp.N, sp.K, sp.batch, want_dt)) {
+        // MN-major B (N contiguous): SWIZZLE_128B rows of MNB = 64 16-bit elements
+        // along N, BK k-rows per block (tcgen05 takes MN-major operands for the
+        // 16-bit kinds only: kind::tf32 B in this layout goes through the gather)
         p.b_loader = LD_TMA_MN;
-        if (sp.N % 64 == 0 && !std::getenv("TMB_NO_MN4D")) {
-          // {64 n, K, N/64 n-blocks, batch}: one box per slot lands the BN/64 column
-          // blocks at 8 KB strides, the layout the per-block boxes produced
+        const int bes = esize(want_dt);
+        const uint64_t mnb = 128 / bes;
+        if (sp.N % mnb == 0 && !std::getenv("TMB_NO_MN4D")) {
+          // {MNB n, K, N/MNB n-blocks, batch}: one box per slot lands the BN/MNB column
+          // blocks at BK*128-byte strides, the layout the per-block boxes produced
           p.b_mn4d = 1;
-          const uint64_t dims[4] = {64, (uint64_t)sp.K, (uint64_t)(sp.N / 64), (uint64_t)sp.batch};
-          const uint64_t strides[3] = {(uint64_t)(f.c1 * 2), 128,
-                                       (uint64_t)(std::max<int64_t>(f.c2, f.c1 * sp.K) * 2)};
-          const uint32_t box[4] = {64u, (uint32_t)BK, (uint32_t)(bn_cta / 64), 1u};
-          make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * 2, opb->dtype, 4, dims, strides, box);
+          const uint64_t dims[4] = {mnb, (uint64_t)sp.K, (uint64_t)(sp.N / mnb), (uint64_t)sp.batch};
+          const uint64_t strides[3] = {(uint64_t)(f.c1 * bes), 128,
+                                       (uint64_t)(std::max<int64_t>(f.c2, f.c1 * sp.K) * bes)};
+          const uint32_t box[4] = {(uint32_t)mnb, (uint32_t)BK, (uint32_t)(bn_cta / mnb), 1u};
+          make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * bes, opb->dtype, 4, dims, strides, box);
         } else {
           p.b_mn4d = 0;
           const uint64_t dims[3] = {(uint64_t)sp.N, (uint64_t)sp.K, (uint64_t)sp.batch};
-          const uint64_t strides[2] = {(uint64_t)(f.c1 * 2), (uint64_t)(std::max<int64_t>(f.c2, f.c1 * sp.K) * 2)};
-          const uint32_t box[3] = {64u, (uint32_t)BK, 1u};
-          make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * 2, opb->dtype, 3, dims, strides, box);
+          const uint64_t strides[2] = {(uint64_t)(f.c1 * bes), (uint64_t)(std::max<int64_t>(f.c2, f.c1 * sp.K) * bes)};
+          const uint32_t box[3] = {(uint32_t)mnb, (uint32_t)BK, 1u};
+          make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * bes, opb->dtype, 3, dims, strides, box);
         }
       } else {
         p.b_loader = LD_GATHER;
@@ -1146,8 +1152,10 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
           p.a_loader == LD_IM2COL_G8 ||
           p.b_loader == LD_FILTER_GATHER || sp.b.kind == OperandPlan::ConvFilter)
         fail_unsupported("math=fp32_simt supports matrix operands only (conv im2col is not supported on this path)");
-      k.bn = 128;
-      p.tiles_n = static_cast<int32_t>((sp.N + 127) / 128);
+      // 128x128 tiles (the paper's mapping), or 128x64 when block_n asks for it
+      k.bn = plan.cfg.block_n <= 64 ? 64 : 128;
+      k.stages = plan.cfg.block_k == 16 ? 16 : 8;  // K-tile depth: the spec's block_k 16, else the paper's 8
+      p.tiles_n = static_cast<int32_t>((sp.N + k.bn - 1) / k.bn);
       p.tiles_m = static_cast<int32_t>((sp.M + 127) / 128);
     }
     // ---- epilogue

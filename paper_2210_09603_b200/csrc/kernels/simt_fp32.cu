@@ -1,6 +1,6 @@
 // fp32 CUDA-core GEMM scheduled with the paper's task mappings (K4a).
 //
-// Block tile 128x128x8, 256 threads.  Every index in this kernel comes from a
+// Block tile 128x128x8 (or 128x64x8 when the 128x128 grid under-fills the SMs), 256 threads.  Every index in this kernel comes from a
 // task mapping (taskmap.cuh, the algebra of proj/src/mapping.cpp):
 //   compute:  spatial(4,2) * repeat(2,2) * spatial(4,8) * repeat(4,4)
 //             (Hidet's CUDA-core matmul mapping): 256
@@ -24,15 +24,35 @@
 namespace tmb {
 namespace {
 
-using ComputeMap = tm::Chain<tm::Spatial<4, 2>, tm::Repeat<2, 2>, tm::Spatial<4, 8>, tm::Repeat<4, 4>>;
-using LoadA = tm::Compose<tm::Repeat<4, 1>, tm::Spatial<32, 8>>;
-using LoadB = tm::Compose<tm::Repeat<1, 4>, tm::Spatial<8, 32>>;
+// BN = 128: the paper's mapping; BN = 64 (twice the CTAs for small grids, e.g.
+// config 1's 1024^2 output = 64 tiles of 128^2 on 148 SMs): one repeat atom
+// halved along N.
+// K-tile depth TBK = 8 (the paper's) or 16: the loads repeat TBK/8 times along k.
+template <int BN, int TBK>
+struct SimtMaps;
+template <int TBK>
+struct SimtMaps<128, TBK> {
+  using Compute = tm::Chain<tm::Spatial<4, 2>, tm::Repeat<2, 2>, tm::Spatial<4, 8>, tm::Repeat<4, 4>>;
+  using LoadA = tm::Compose<tm::Repeat<4, TBK / 8>, tm::Spatial<32, 8>>;
+  using LoadB = tm::Compose<tm::Repeat<TBK / 8, 4>, tm::Spatial<8, 32>>;
+};
+template <int TBK>
+struct SimtMaps<64, TBK> {
+  using Compute = tm::Chain<tm::Spatial<4, 2>, tm::Repeat<2, 1>, tm::Spatial<4, 8>, tm::Repeat<4, 4>>;
+  using LoadA = tm::Compose<tm::Repeat<4, TBK / 8>, tm::Spatial<32, 8>>;
+  using LoadB = tm::Compose<tm::Repeat<TBK / 8, 2>, tm::Spatial<8, 32>>;
+};
+using ComputeMap = SimtMaps<128, 8>::Compute;
+using LoadA = SimtMaps<128, 8>::LoadA;
+using LoadB = SimtMaps<128, 8>::LoadB;
 static_assert(ComputeMap::workers == 256 && ComputeMap::tasks == 64, "CUDA-core mapping shape");
 static_assert(ComputeMap::dim(0) == 128 && ComputeMap::dim(1) == 128, "covers the 128x128 tile");
+static_assert(SimtMaps<64, 8>::Compute::workers == 256 && SimtMaps<64, 8>::Compute::dim(1) == 64, "128x64 tile");
+static_assert(SimtMaps<128, 16>::LoadA::dim(1) == 16 && SimtMaps<128, 16>::LoadB::dim(0) == 16, "16-deep K tile");
 static_assert(LoadA::workers == 256 && LoadA::dim(0) == 128 && LoadA::dim(1) == 8, "A tile 128x8");
 static_assert(LoadB::workers == 256 && LoadB::dim(0) == 8 && LoadB::dim(1) == 128, "B tile 8x128");
 
-constexpr int TBM = 128, TBN = 128, TBK = 8;
+constexpr int TBM = 128;
 
 __device__ __forceinline__ float ld_elem(const void* base, int64_t idx, int32_t dt) {
   if (dt == DT_F32) return __ldg(reinterpret_cast<const float*>(base) + idx);
@@ -109,76 +129,99 @@ __device__ float epilogue1(const GemmParams& p, float v, int64_t r, int64_t c, i
   return v;
 }
 
+template <int TBN, int TBK>
 __global__ void __launch_bounds__(256) simt_gemm_kernel(const __grid_constant__ GemmParams p) {
-  __shared__ float As[2][TBK][TBM + 4];  // A tile stored k-major (transposed) for fragment reads
-  __shared__ float Bs[2][TBK][TBN + 4];
+  using CMap = typename SimtMaps<TBN, TBK>::Compute;
+  using AMap = typename SimtMaps<TBN, TBK>::LoadA;
+  using BMap = typename SimtMaps<TBN, TBK>::LoadB;
+  constexpr int CN = TBN / 16;  // columns per thread (4 per repeat(4,4) block, TBN / 64 blocks)
+  __shared__ __align__(16) float As[2][TBK][TBM + 4];  // A tile stored k-major (transposed) for fragment reads
+  __shared__ __align__(16) float Bs[2][TBK][TBN + 4];
   const uint32_t t = threadIdx.x;
-  // tile of this block: task mapping over (batch, tile_m, tile_n) as in the tcgen05 kernel
-  int32_t tc[tm::kMaxRank];
-  const int64_t tid = blockIdx.x;
   const int tiles_mn = p.tiles_m * p.tiles_n;
-  const int b = static_cast<int>(tid / tiles_mn);
-  const int tm_ = static_cast<int>((tid % tiles_mn) / p.tiles_n), tn = static_cast<int>(tid % p.tiles_n);
-  (void)tc;
+  const int b = static_cast<int>(blockIdx.x / tiles_mn);
+  const int tm_ = static_cast<int>((blockIdx.x % tiles_mn) / p.tiles_n), tn = static_cast<int>(blockIdx.x % p.tiles_n);
   const int64_t m0 = int64_t(tm_) * TBM, n0 = int64_t(tn) * TBN;
   const Strided& A = p.a;
   const Strided& B = p.b;
-
-  float ra[LoadA::tasks], rb[LoadB::tasks];
-  auto load_tiles = [&](int k0) {
+  // Each thread's load tasks touch fixed rows (A) / columns (B) and fixed k offsets
+  // inside a K-tile: their element offsets are computed once, and a K-tile only
+  // adds k0 * s_k (no per-element div/mod of the strided address map).
+  int64_t abase[AMap::tasks], bbase[BMap::tasks];
+  int ak[AMap::tasks], bk[BMap::tasks];
+  bool aok[AMap::tasks], bok[BMap::tasks];
 #pragma unroll
-    for (uint32_t i = 0; i < LoadA::tasks; ++i) {
-      int c[2];
-      LoadA::task(t, i, c);  // (m, k) within the tile
-      const int64_t m = m0 + c[0], k = k0 + c[1];
-      ra[i] = (m < p.M && k < p.K)
-                  ? ld_operand(A, row_part(A.P, A.s_hi, A.s_lo, m) + k * A.s_k + b * A.s_batch + A.offset)
-                  : 0.f;
+  for (uint32_t i = 0; i < AMap::tasks; ++i) {
+    int c[2];
+    AMap::task(t, i, c);  // (m, k) within the tile
+    const int64_t m = m0 + c[0];
+    aok[i] = m < p.M;
+    abase[i] = (aok[i] ? row_part(A.P, A.s_hi, A.s_lo, m) : 0) + c[1] * A.s_k + b * A.s_batch + A.offset;
+    ak[i] = c[1];
+  }
+#pragma unroll
+  for (uint32_t i = 0; i < BMap::tasks; ++i) {
+    int c[2];
+    BMap::task(t, i, c);  // (k, n) within the tile
+    const int64_t n = n0 + c[1];
+    bok[i] = n < p.N;
+    bbase[i] = (bok[i] ? row_part(B.P, B.s_hi, B.s_lo, n) : 0) + c[0] * B.s_k + b * B.s_batch + B.offset;
+    bk[i] = c[0];
+  }
+  const bool plain = A.n_pre == 0 && B.n_pre == 0 && A.dtype == DT_F32 && B.dtype == DT_F32;
+  float ra[AMap::tasks], rb[BMap::tasks];
+  auto load_tiles = [&](int k0) {
+    const int64_t ka = int64_t(k0) * A.s_k, kb = int64_t(k0) * B.s_k;
+#pragma unroll
+    for (uint32_t i = 0; i < AMap::tasks; ++i) {
+      const bool ok = aok[i] && k0 + ak[i] < p.K;
+      ra[i] = !ok ? 0.f : plain ? __ldg(reinterpret_cast<const float*>(A.ptr) + abase[i] + ka) : ld_operand(A, abase[i] + ka);
     }
 #pragma unroll
-    for (uint32_t i = 0; i < LoadB::tasks; ++i) {
-      int c[2];
-      LoadB::task(t, i, c);  // (k, n) within the tile
-      const int64_t k = k0 + c[0], n = n0 + c[1];
-      rb[i] = (n < p.N && k < p.K)
-                  ? ld_operand(B, row_part(B.P, B.s_hi, B.s_lo, n) + k * B.s_k + b * B.s_batch + B.offset)
-                  : 0.f;
+    for (uint32_t i = 0; i < BMap::tasks; ++i) {
+      const bool ok = bok[i] && k0 + bk[i] < p.K;
+      rb[i] = !ok ? 0.f : plain ? __ldg(reinterpret_cast<const float*>(B.ptr) + bbase[i] + kb) : ld_operand(B, bbase[i] + kb);
     }
   };
   auto store_tiles = [&](int buf) {
 #pragma unroll
-    for (uint32_t i = 0; i < LoadA::tasks; ++i) {
+    for (uint32_t i = 0; i < AMap::tasks; ++i) {
       int c[2];
-      LoadA::task(t, i, c);
+      AMap::task(t, i, c);
       As[buf][c[1]][c[0]] = ra[i];
     }
 #pragma unroll
-    for (uint32_t i = 0; i < LoadB::tasks; ++i) {
+    for (uint32_t i = 0; i < BMap::tasks; ++i) {
       int c[2];
-      LoadB::task(t, i, c);
+      BMap::task(t, i, c);
       Bs[buf][c[0]][c[1]] = rb[i];
     }
   };
 
-  // this thread's 8 distinct rows / 8 distinct columns of the compute mapping:
-  // tasks i = (r1m*2 + r1n)*16 + r2m*4 + r2n (repeat atoms, outer first)
-  int rows[8], cols[8];
+  // this thread's rows / columns under the compute mapping: the innermost
+  // repeat(4,4) atom makes each group of 4 consecutive, so fragments are read
+  // as float4 (rows: 2 groups; columns: TBN/64 groups)
+  int rows[8], cols[CN];
 #pragma unroll
   for (int r1 = 0; r1 < 2; ++r1)
 #pragma unroll
     for (int r2 = 0; r2 < 4; ++r2) {
       int c[2];
-      ComputeMap::task(t, (r1 * 2) * 16 + r2 * 4, c);
+      CMap::task(t, (r1 * (TBN / 64)) * 16 + r2 * 4, c);
       rows[r1 * 4 + r2] = c[0];
-      ComputeMap::task(t, r1 * 16 + r2, c);
-      cols[r1 * 4 + r2] = c[1];
     }
+#pragma unroll
+  for (int j = 0; j < CN; ++j) {
+    int c[2];
+    CMap::task(t, (j / 4) * 16 + (j % 4), c);
+    cols[j] = c[1];
+  }
 
-  float acc[8][8];
+  float acc[8][CN];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    for (int j = 0; j < CN; ++j) acc[i][j] = 0.f;
 
   const int ktiles = (p.K + TBK - 1) / TBK;
   load_tiles(0);
@@ -189,15 +232,21 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const __grid_constant__ 
     if (kt + 1 < ktiles) load_tiles((kt + 1) * TBK);  // Fig. 6: preload next tile into registers
 #pragma unroll
     for (int k = 0; k < TBK; ++k) {
-      float af[8], bf[8];
+      float af[8], bf[CN];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) af[i] = As[buf][k][rows[i]];
+      for (int g = 0; g < 2; ++g) {
+        const float4 v = *reinterpret_cast<const float4*>(&As[buf][k][rows[4 * g]]);
+        af[4 * g] = v.x; af[4 * g + 1] = v.y; af[4 * g + 2] = v.z; af[4 * g + 3] = v.w;
+      }
 #pragma unroll
-      for (int j = 0; j < 8; ++j) bf[j] = Bs[buf][k][cols[j]];
+      for (int g = 0; g < CN / 4; ++g) {
+        const float4 v = *reinterpret_cast<const float4*>(&Bs[buf][k][cols[4 * g]]);
+        bf[4 * g] = v.x; bf[4 * g + 1] = v.y; bf[4 * g + 2] = v.z; bf[4 * g + 3] = v.w;
+      }
 #pragma unroll
       for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(af[i], bf[j], acc[i][j]);
+        for (int j = 0; j < CN; ++j) acc[i][j] = fmaf(af[i], bf[j], acc[i][j]);
     }
     if (kt + 1 < ktiles) {
       store_tiles(buf ^ 1);  // commit the staged tile to the other buffer
@@ -211,7 +260,7 @@ __global__ void __launch_bounds__(256) simt_gemm_kernel(const __grid_constant__ 
     if (r >= p.M) continue;
     const int64_t obase = row_part(p.out_a.P, p.out_a.s_hi, p.out_a.s_lo, r) + b * p.out_a.s_batch + p.out_a.offset;
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < CN; ++j) {
       const int64_t c = n0 + cols[j];
       if (c >= p.N) continue;
       const float v = epilogue1(p, acc[i][j], r, c, b);
@@ -243,7 +292,15 @@ int kernel_mapping_assign(int which, uint32_t worker, int* buf, int cap) {
 void launch_simt(const BoundKernel& k, void* stream) {
   const GemmParams& p = k.p;
   const int64_t blocks = int64_t(p.batch) * p.tiles_m * p.tiles_n;
-  simt_gemm_kernel<<<static_cast<unsigned>(blocks), 256, 0, static_cast<cudaStream_t>(stream)>>>(p);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const unsigned g = static_cast<unsigned>(blocks);
+  if (k.bn == 64) {
+    if (k.stages == 16) simt_gemm_kernel<64, 16><<<g, 256, 0, s>>>(p);
+    else simt_gemm_kernel<64, 8><<<g, 256, 0, s>>>(p);
+  } else {
+    if (k.stages == 16) simt_gemm_kernel<128, 16><<<g, 256, 0, s>>>(p);
+    else simt_gemm_kernel<128, 8><<<g, 256, 0, s>>>(p);
+  }
 }
 
 }  // namespace tmb

@@ -213,6 +213,32 @@ def test_fp32_cuda_core_exact_int(mnk):
     assert np.array_equal(got["D"], want["D"])
 
 
+@pytest.mark.parametrize("mnk,bn,bk", [((256, 256, 256), 64, 8), ((2039, 67, 131), 64, 16), ((1024, 1024, 1024), 64, 16),
+                                       ((300, 200, 77), 128, 16), ((129, 130, 15), 128, 8)])
+def test_fp32_cuda_core_tile_variants_exact_int(mnk, bn, bk):
+    """The 128x64 CUDA-core tile (spatial(4,2)*repeat(2,1)*spatial(4,8)*repeat(4,4)) and ragged edges."""
+    m, n, k = mnk
+    a, b, bias = _matmul_case(m, n, k, True, 81)
+    dag = matmul_epilogue_dag(m, n, k, DType.I32)
+    got, _ = run(dag, {"A": dev(a, "f32"), "B": dev(b, "f32"), "Bias": dev(bias, "f32")}, {"D": (m, n)},
+                 cfg=ScheduleConfig(math="fp32_simt", block_n=bn, block_k=bk))
+    assert np.array_equal(got["D"], port.matmul_bias_relu(a, b, bias))
+
+
+@pytest.mark.parametrize("bn,sk", [(128, 1), (256, 2)])
+def test_matmul_tf32_row_major_b(bn, sk):
+    """kind::tf32 with B [K,N] row-major (MN-major fp32: tcgen05 takes MN-major only for 16-bit
+    kinds, so B is gathered and transposed by the loader warps)."""
+    m, n, k = 512, 384, 256
+    rng = port.Rng(13)
+    a, b = rounded(rng.tensor((m, k)), "tf32"), rounded(rng.tensor((k, n)), "tf32")
+    bias = rounded(rng.tensor((n,)), "f32")
+    dag = matmul_epilogue_dag(m, n, k)
+    got, _ = run(dag, {"A": dev(a, "f32"), "B": dev(b, "f32"), "Bias": dev(bias, "f32")}, {"D": (m, n)},
+                 cfg=ScheduleConfig(math="tf32", block_n=bn, split_k=sk))
+    assert port.max_rel_error(got["D"], port.matmul_bias_relu(a, b, bias)) <= 1e-4
+
+
 def test_matmul_tf32():
     m, n, k = 512, 384, 256
     rng = port.Rng(12)
