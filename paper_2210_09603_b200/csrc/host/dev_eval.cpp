@@ -45,8 +45,6 @@ int64_t span_of(const tm_tensor& t) {
   return s;
 }
 
-namespace {
-
 struct Compiler {
   std::map<std::string, int> vars;       // axis name -> var slot
   std::map<std::string, int> tensor_ix;  // tensor name -> TensorRef slot
@@ -132,6 +130,20 @@ struct Compiler {
     fail("device evaluator: unknown expression kind");
   }
 };
+
+Program compile_program(const Expr& e, const std::vector<std::string>& var_names) {
+  Compiler c;
+  for (size_t i = 0; i < var_names.size(); ++i) c.vars[var_names[i]] = static_cast<int>(i);
+  c.compile(e);
+  if (c.max_depth > kMaxStack) fail_unsupported("expression is too deep for the device interpreter (stack ", c.max_depth, ")");
+  Program p;
+  p.code = std::move(c.code);
+  p.tensors = std::move(c.tensors);
+  p.tables = std::move(c.tables);
+  return p;
+}
+
+namespace {
 
 int store_of(int32_t dt) { return dt == TM_F32 ? ST_F32 : dt == TM_BF16 ? ST_BF16 : ST_F16; }
 

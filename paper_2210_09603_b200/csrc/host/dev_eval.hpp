@@ -66,6 +66,16 @@ class DagEval {
   std::vector<std::shared_ptr<DeviceBuffer>> keep_;
 };
 
+// Stack bytecode of one expression tree; variable slot i is var_names[i], load
+// slot j reads tensors[j].  Shared by this interpreter and the product's
+// rule-based / reduce kernels (rule.cpp).
+struct Program {
+  std::vector<Ins> code;
+  std::vector<std::string> tensors;
+  std::vector<int64_t> tables;
+};
+Program compile_program(const taskmap::Expr& e, const std::vector<std::string>& var_names);
+
 // True when every computed node keeps integer-valued inputs exact in fp32
 // (no exp/sqrt/float division, float constants exact in bf16): the integer
 // verification trial then requires bit-identical outputs.

@@ -22,6 +22,7 @@
 
 #include "json.hpp"
 #include "plan.hpp"
+#include "dev_eval.hpp"
 
 namespace tmb {
 
@@ -106,10 +107,34 @@ std::vector<taskmap::FusedSubgraph> taskmap::partition(const taskmap::ComputeDAG
     sg.output = cur;
     out.push_back(std::move(sg));
   }
-  // anchor-free remainder: rule-based injective kernels
+  // anchor-free remainder: rule-based injective kernels.  A
+  // remainder node used once, by another remainder node, and not a DAG output is
+  // inlined into its consumer (listed as that subgraph's prologue); every other
+  // remainder node roots one kernel.
+  std::set<std::string> rem;
+  for (const auto& n : dag.nodes)
+    if (n.kind == NodeKind::GridCompute && !taken.count(n.name)) rem.insert(n.name);
+  auto inlined = [&](const std::string& n) {
+    return rem.count(n) && single_use(n) && rem.count(cons[n][0]);
+  };
   for (const auto& n : dag.nodes) {
-    if (n.kind != NodeKind::GridCompute || taken.count(n.name)) continue;
+    if (!rem.count(n.name) || inlined(n.name)) continue;
     FusedSubgraph sg;
+    // producers spliced into this root, innermost first
+    std::vector<std::string> stack = {n.name}, order;
+    std::set<std::string> seen;
+    while (!stack.empty()) {
+      const std::string cur = stack.back();
+      stack.pop_back();
+      std::vector<Expr> ls;
+      collect_loads(dag.at(cur).value, ls);
+      for (const auto& l : ls)
+        if (inlined(l->name) && seen.insert(l->name).second) {
+          order.push_back(l->name);
+          stack.push_back(l->name);
+        }
+    }
+    for (auto it = order.rbegin(); it != order.rend(); ++it) sg.prologue.push_back(*it);
     sg.epilogue.push_back(n.name);
     sg.output = n.name;
     out.push_back(std::move(sg));
@@ -577,6 +602,13 @@ SubgraphPlan lower_subgraph(const ComputeDAG& dag, const FusedSubgraph& sg) {
 
 std::string SubgraphPlan::describe() const {
   std::ostringstream o;
+  if (kind == Rule) {
+    o << "{\"kind\":" << tmjson::quote(sg.anchor.empty() ? "rule" : "reduce") << ",\"root\":" << tmjson::quote(rule_node)
+      << ",\"elements\":" << M << ",\"reduce\":" << K << ",\"inlined\":[";
+    for (size_t i = 0; i < sg.prologue.size(); ++i) o << (i ? "," : "") << tmjson::quote(sg.prologue[i]);
+    o << "],\"expr\":" << tmjson::quote(expr_to_text(rule_expr)) << "}";
+    return o.str();
+  }
   auto idxs = [](const AddrExpr& a) {
     std::string s = a.tensor + "[";
     for (size_t i = 0; i < a.idx.size(); ++i) s += (i ? ", " : "") + expr_to_text(a.idx[i]);
@@ -589,7 +621,7 @@ std::string SubgraphPlan::describe() const {
     for (const auto& st : p.pre) s += " |> op" + std::to_string(st.kind) + "(" + std::to_string(st.c) + ")";
     return s;
   };
-  o << "{\"anchor\":" << tmjson::quote(sg.anchor) << ",\"M\":" << M << ",\"N\":" << N << ",\"K\":" << K
+  o << "{\"kind\":\"gemm\",\"anchor\":" << tmjson::quote(sg.anchor) << ",\"M\":" << M << ",\"N\":" << N << ",\"K\":" << K
     << ",\"batch\":" << batch << ",\"A\":" << tmjson::quote(opd(a)) << ",\"B\":" << tmjson::quote(opd(b))
     << ",\"prologue\":[";
   for (size_t i = 0; i < sg.prologue.size(); ++i) o << (i ? "," : "") << tmjson::quote(sg.prologue[i]);
@@ -605,15 +637,214 @@ std::string SubgraphPlan::describe() const {
   return o.str();
 }
 
+namespace {
+
+// The reduction anchor is a matrix product the GEMM templates lower (one sum
+// axis over the product of two loads, each operand owning one spatial axis, at
+// most one shared batch axis): the checks lower_subgraph enforces.
+bool matmul_anchor(const TensorNode& r) {
+  if (r.combiner != Combiner::Sum || r.reduce_axes.size() != 1 || (r.axes.size() != 2 && r.axes.size() != 3)) return false;
+  const Expr& v = r.value;
+  if (v->kind != ExprKind::Binary || v->bop != BinOp::Mul || v->args[0]->kind != ExprKind::Load ||
+      v->args[1]->kind != ExprKind::Load)
+    return false;
+  auto uses = [&](const Expr& l, const std::string& ax) {
+    return std::any_of(l->args.begin(), l->args.end(), [&](const Expr& i) { return contains_var(i, ax); });
+  };
+  int own0 = 0, own1 = 0, bat = 0;
+  for (const auto& ax : r.axes) {
+    const bool u0 = uses(v->args[0], ax.name), u1 = uses(v->args[1], ax.name);
+    if (u0 && u1) ++bat;
+    else if (u0) ++own0;
+    else if (u1) ++own1;
+    else return false;
+  }
+  const std::string k = r.reduce_axes[0].name;
+  return own0 == 1 && own1 == 1 && bat <= 1 && uses(v->args[0], k) && uses(v->args[1], k);
+}
+
+// A prologue node the operand loaders can apply: a pure re-index of a graph
+// input, or an elementwise chain over one element of one graph input with
+// constant side operands (lower_subgraph's arithmetic prologue).
+bool loader_prologue(const ComputeDAG& dag, const TensorNode& s) {
+  if (s.value->kind == ExprKind::Load) return dag.at(s.value->name).kind == NodeKind::Input;
+  std::vector<Expr> lds;
+  collect_loads(s.value, lds);
+  if (lds.size() != 1 || dag.at(lds[0]->name).kind != NodeKind::Input) return false;
+  std::function<bool(const Expr&)> chain = [&](const Expr& e) -> bool {
+    if (e->kind == ExprKind::Load) return true;
+    if (e->kind == ExprKind::Unary)
+      return e->uop != UnOp::CastI32 && chain(e->args[0]);
+    if (e->kind == ExprKind::Binary) {
+      std::vector<Expr> l0, l1;
+      collect_loads(e->args[0], l0);
+      collect_loads(e->args[1], l1);
+      if (l0.empty() == l1.empty()) return false;
+      const Expr side = fold(l0.empty() ? e->args[0] : e->args[1]);
+      if (side->kind != ExprKind::FloatImm && side->kind != ExprKind::IntImm) return false;
+      switch (e->bop) {
+        case BinOp::Add: case BinOp::Sub: case BinOp::Mul: case BinOp::Div: case BinOp::Max: case BinOp::Min: break;
+        default: return false;
+      }
+      return chain(l0.empty() ? e->args[1] : e->args[0]);
+    }
+    return false;
+  };
+  if (!chain(s.value)) return false;
+  int ops = 0;  // the loader applies at most kMaxPreOps ops
+  std::function<void(const Expr&)> count = [&](const Expr& e) {
+    if (e->kind == ExprKind::Unary && e->uop != UnOp::CastF32) ++ops;
+    if (e->kind == ExprKind::Binary) ++ops;
+    for (const auto& a : e->args)
+      if (a->kind != ExprKind::Load) count(a);
+  };
+  count(s.value);
+  return ops <= kMaxPreOps;
+}
+
+// rule_based_schedule / reduce_template lowering:
+// the root's value with the inlined producers spliced in (rewrite_loads, the
+// fuse_prologue primitive).
+SubgraphPlan lower_rule(const ComputeDAG& dag, const std::string& root, const std::vector<std::string>& inlined) {
+  SubgraphPlan sp;
+  sp.kind = SubgraphPlan::Rule;
+  sp.rule_node = root;
+  sp.sg.output = root;
+  sp.sg.prologue = inlined;
+  const TensorNode& n = dag.at(root);
+  if (n.axes.size() > static_cast<size_t>(ev::kMaxRank) || n.reduce_axes.size() > static_cast<size_t>(ev::kMaxRank) ||
+      n.axes.size() + n.reduce_axes.size() > static_cast<size_t>(ev::kMaxVars))
+    fail_unsupported("rule kernel '", n.name, "': more than ", ev::kMaxRank, " axes");
+  if (n.kind == NodeKind::GridReduce) sp.sg.anchor = root;
+  else sp.sg.epilogue.push_back(root);
+  const std::set<std::string> inl(inlined.begin(), inlined.end());
+  Expr e = n.value;
+  for (int round = 0; round < 256; ++round) {
+    bool changed = false;
+    e = rewrite_loads(e, [&](const ExprNode& ld) -> std::optional<Expr> {
+      if (!inl.count(ld.name)) return std::nullopt;
+      const TensorNode& p = dag.at(ld.name);
+      if (p.kind != NodeKind::GridCompute) fail("rule kernel: cannot inline reduction '", p.name, "'");
+      std::map<std::string, Expr> m;
+      for (size_t d = 0; d < p.axes.size(); ++d) m[p.axes[d].name] = ld.args[d];
+      changed = true;
+      return substitute(p.value, m);
+    });
+    if (!changed) break;
+  }
+  sp.rule_expr = fold(e);
+  int64_t m = 1;
+  for (const auto& a : n.axes) m *= a.extent;
+  sp.M = m;
+  sp.N = 1;
+  sp.K = 1;
+  for (const auto& a : n.reduce_axes) sp.K *= a.extent;
+  return sp;
+}
+
+}  // namespace
+
 std::unique_ptr<Plan> build_plan(const ComputeDAG& dag, const ScheduleConfig& cfg, int device) {
   auto plan = std::make_unique<Plan>();
   plan->dag = dag;
   plan->cfg = cfg;
   plan->device = device;
   std::set<std::string> produced;
-  for (const auto& sg : partition(dag)) {
-    plan->kernels.push_back(lower_subgraph(dag, sg));
+  for (const auto& sg0 : partition(dag)) {
+    FusedSubgraph sg = sg0;
+    if (sg.anchor.empty()) {
+      // anchor-free: one rule-based kernel, the prologue nodes inlined
+      plan->kernels.push_back(lower_rule(dag, sg.output, sg.prologue));
+      produced.insert(sg.output);
+      continue;
+    }
+    const TensorNode& r = dag.at(sg.anchor);
+    if (!matmul_anchor(r)) {
+      // reduce template for the anchor (its injective prologues inlined), then the
+      // epilogue chain as one rule-based kernel reading the materialised reduction
+      plan->kernels.push_back(lower_rule(dag, sg.anchor, sg.prologue));
+      produced.insert(sg.anchor);
+      if (!sg.epilogue.empty()) {
+        std::vector<std::string> chain(sg.epilogue.begin(), sg.epilogue.end() - 1);
+        plan->kernels.push_back(lower_rule(dag, sg.output, chain));
+        produced.insert(sg.output);
+      }
+      continue;
+    }
+    // matrix-product anchor: prologue nodes the loaders cannot apply (they read
+    // intermediates or several tensors) are materialised by rule kernels first
+    bool conv = false;
+    for (const auto& pn : sg.prologue) {
+      ConvInfo ci{};
+      conv = conv || match_im2col(dag, dag.at(pn), ci);
+    }
+    if (!conv) {
+      std::vector<std::string> keep;
+      for (const auto& pn : sg.prologue) {
+        if (loader_prologue(dag, dag.at(pn))) {
+          keep.push_back(pn);
+        } else {
+          plan->kernels.push_back(lower_rule(dag, pn, {}));
+          produced.insert(pn);
+        }
+      }
+      sg.prologue = keep;
+    }
+    // an epilogue chain the register program cannot express is cut where it
+    // stops lowering; the cut-off consumers run as rule-based kernels
+    std::vector<std::string> cut;
+    for (;;) {
+      try {
+        plan->kernels.push_back(lower_subgraph(dag, sg));
+        break;
+      } catch (const UnsupportedError&) {
+        if (sg.epilogue.empty()) throw;
+        cut.insert(cut.begin(), sg.epilogue.back());
+        sg.epilogue.pop_back();
+        sg.output = sg.epilogue.empty() ? sg.anchor : sg.epilogue.back();
+      }
+    }
     produced.insert(sg.output);
+    if (!cut.empty()) {
+      std::vector<std::string> chain(cut.begin(), cut.end() - 1);
+      plan->kernels.push_back(lower_rule(dag, cut.back(), chain));
+      produced.insert(cut.back());
+    }
+  }
+  // kernels in dependency order: anchors come out of partition first and the
+  // anchor-free (rule) kernels after them, but a reduction may read an
+  // anchor-free node (softmax: sum_j exp(S - max)); stable topological order
+  {
+    std::vector<SubgraphPlan> todo = std::move(plan->kernels), sorted;
+    std::set<std::string> done;
+    for (const auto& n : dag.nodes)
+      if (n.kind == NodeKind::Input) done.insert(n.name);
+    auto reads = [&](const SubgraphPlan& sp) {
+      std::set<std::string> mem, out;
+      if (!sp.sg.anchor.empty()) mem.insert(sp.sg.anchor);
+      for (const auto& x : sp.sg.prologue) mem.insert(x);
+      for (const auto& x : sp.sg.epilogue) mem.insert(x);
+      if (!sp.rule_node.empty()) mem.insert(sp.rule_node);
+      for (const auto& m : mem) {
+        std::vector<Expr> ls;
+        collect_loads(dag.at(m).value, ls);
+        for (const auto& l : ls)
+          if (!mem.count(l->name)) out.insert(l->name);
+      }
+      return out;
+    };
+    while (!todo.empty()) {
+      size_t pick = todo.size();
+      for (size_t i = 0; i < todo.size() && pick == todo.size(); ++i) {
+        const auto r = reads(todo[i]);
+        if (std::all_of(r.begin(), r.end(), [&](const std::string& x) { return done.count(x) > 0; })) pick = i;
+      }
+      if (pick == todo.size()) fail("fused kernels have a cyclic dependency");
+      done.insert(todo[pick].sg.output);
+      sorted.push_back(std::move(todo[pick]));
+      todo.erase(todo.begin() + static_cast<std::ptrdiff_t>(pick));
+    }
+    plan->kernels = std::move(sorted);
   }
   for (const auto& o : dag.outputs)
     if (!produced.count(o)) fail("output '", o, "' is not produced by a fused kernel");
@@ -893,6 +1124,80 @@ bool bind_rowband(const SubgraphPlan& sp, const std::map<std::string, tm_tensor>
   }
   return true;
 }
+// Rule / reduce kernel binding: bytecode + tensor references in one device
+// blob owned by the exec; the output is the root node's bound (or
+// plan-owned intermediate) tensor.
+BoundKernel bind_rule(const Plan& plan, const SubgraphPlan& sp, const std::map<std::string, tm_tensor>& env, Exec& ex,
+                      int sms) {
+  const ComputeDAG& dag = plan.dag;
+  const TensorNode& n = dag.at(sp.rule_node);
+  if (n.axes.size() > static_cast<size_t>(ev::kMaxRank) || n.reduce_axes.size() > static_cast<size_t>(ev::kMaxRank) ||
+      n.axes.size() + n.reduce_axes.size() > static_cast<size_t>(ev::kMaxVars))
+    fail_unsupported("rule kernel '", n.name, "': too many axes");
+  std::vector<std::string> vars;
+  for (const auto& a : n.axes) vars.push_back(a.name);
+  for (const auto& a : n.reduce_axes) vars.push_back(a.name);
+  const ev::Program prog = ev::compile_program(sp.rule_expr, vars);
+  auto ref_of = [&](const std::string& name) {
+    const tm_tensor& t = lookup(env, name);
+    const TensorNode& tn = dag.at(name);
+    if (t.rank > ev::kMaxRank) fail_unsupported("tensor '", name, "' has too many dims for a rule kernel");
+    ev::TensorRef r{};
+    r.ptr = t.data;
+    r.store = t.dtype == TM_F32 ? ev::ST_F32 : t.dtype == TM_BF16 ? ev::ST_BF16 : ev::ST_F16;
+    r.is_float = tn.dtype == taskmap::DType::F32;
+    r.rank = t.rank;
+    for (int d = 0; d < t.rank; ++d) {
+      r.shape[d] = t.shape[d];
+      r.stride[d] = t.stride[d];
+    }
+    return r;
+  };
+  std::vector<ev::TensorRef> refs;
+  for (const auto& name : prog.tensors) refs.push_back(ref_of(name));
+  const size_t code_b = prog.code.size() * sizeof(ev::Ins), refs_b = refs.size() * sizeof(ev::TensorRef),
+               tab_b = prog.tables.size() * sizeof(int64_t);
+  std::vector<unsigned char> host(code_b + refs_b + tab_b + 64, 0);
+  std::memcpy(host.data(), prog.code.data(), code_b);
+  if (refs_b) std::memcpy(host.data() + code_b, refs.data(), refs_b);
+  if (tab_b) std::memcpy(host.data() + code_b + refs_b, prog.tables.data(), tab_b);
+  void* blob = nullptr;
+  if (cudaMalloc(&blob, host.size()) != cudaSuccess ||
+      cudaMemcpy(blob, host.data(), host.size(), cudaMemcpyHostToDevice) != cudaSuccess)
+    fail_cuda("cudaMalloc/cudaMemcpy failed for a rule-kernel program");
+  ex.scratch.push_back(blob);
+  BoundKernel k{};
+  k.rule = 1;
+  RuleJob& j = k.rj;
+  j.code = static_cast<const ev::Ins*>(blob);
+  j.tensors = reinterpret_cast<const ev::TensorRef*>(static_cast<unsigned char*>(blob) + code_b);
+  j.tables = reinterpret_cast<const int64_t*>(static_cast<unsigned char*>(blob) + code_b + refs_b);
+  j.n_code = static_cast<int32_t>(prog.code.size());
+  j.n_axes = static_cast<int32_t>(n.axes.size());
+  j.n_red = static_cast<int32_t>(n.reduce_axes.size());
+  j.combiner = static_cast<int32_t>(n.combiner);
+  j.is_float = n.dtype == taskmap::DType::F32;
+  j.numel = 1;
+  for (size_t d = 0; d < n.axes.size(); ++d) {
+    j.ext[d] = n.axes[d].extent;
+    j.numel *= n.axes[d].extent;
+  }
+  j.red_numel = 1;
+  for (size_t d = 0; d < n.reduce_axes.size(); ++d) {
+    j.red[d] = n.reduce_axes[d].extent;
+    j.red_numel *= n.reduce_axes[d].extent;
+  }
+  // reduce_template (one CTA per output, tree) for long reductions or few
+  // outputs; the sequential in-thread loop of rule_based_schedule for short ones
+  // over many outputs (reduce extent <= 256 inlines as SeqFor)
+  const bool tree = j.n_red > 0 && (j.red_numel > 256 || j.numel < int64_t(sms) * 64);
+  j.mode = tree ? RULE_TREE : RULE_ELEM;
+  j.out = ref_of(sp.rule_node);
+  k.rule_threads = plan.cfg.threads_per_block > 0 ? plan.cfg.threads_per_block : 128;
+  k.grid = sms;  // launch_rule sizes the grid from the SM count
+  k.bn = 0;
+  return k;
+}
 }  // namespace
 
 int intermediate_dtype(const tm_tensor* inputs, int n_in) {
@@ -951,6 +1256,10 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
   }
   const int sms = num_sms(plan.device);
   for (const auto& sp : plan.kernels) {
+    if (sp.kind == SubgraphPlan::Rule) {
+      ex->kernels.push_back(bind_rule(plan, sp, env, *ex, sms));
+      continue;
+    }
     BoundKernel k{};
     GemmParams& p = k.p;
     p.M = static_cast<int32_t>(sp.M);

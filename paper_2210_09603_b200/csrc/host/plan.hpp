@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "../device/gemm_params.h"
+#include "../device/rule.h"
 #include "taskmap/ir.hpp"
 #include "taskmap/schedule.hpp"
 #include "taskmap_b200.h"
@@ -53,6 +54,13 @@ struct OperandPlan {
 };
 
 struct SubgraphPlan {
+  // Gemm: the task-mapped tcgen05 / CUDA-core matmul template with fused
+  // prologue loaders and epilogue program.  Rule: a rule-based injective kernel
+  // or, when the root is a non-matmul reduction, the reduce template
+  // (rule_kernels.cu); the root's expression has every inlined producer spliced in.
+  enum Kind { Gemm, Rule } kind = Gemm;
+  std::string rule_node;       // Rule: the root node (written to its tensor)
+  taskmap::Expr rule_expr;     // Rule: root value with inlined producers substituted
   taskmap::FusedSubgraph sg;
   int64_t M = 0, N = 0, K = 0, batch = 1;
   OperandPlan a, b;                 // A provides rows, B provides cols
@@ -79,6 +87,9 @@ struct BoundKernel {
   int bn = 128, stages = 4, tf32 = 0, grid = 148, simt = 0, cg = 1;
   int generic = 1;  // 0: compact instantiation (TMA loaders + canonical epilogue only)
   int rowband = 0;  // 1: tm_rowband_kernel (conv_rowband.cuh); tma_a = staged-row map, smem = its layout
+  int rule = 0;     // 1: rule-based / reduce-template kernel (rule_kernels.cu) running `rj`
+  int rule_threads = 128;
+  RuleJob rj{};
   int smem = 0;
   alignas(64) unsigned char tma_a[128];
   alignas(64) unsigned char tma_b[128];
@@ -106,6 +117,7 @@ int rowband_smem(int rows, int rowb, int bbytes, int bn);
 // is f32, fp16 if the 16-bit inputs are all fp16, else bf16
 int intermediate_dtype(const tm_tensor* inputs, int n_in);
 void launch_simt(const BoundKernel& k, void* stream);   // fp32 CUDA-core kernel (simt_fp32.cu)
+void launch_rule(const RuleJob& j, int threads, int sms, void* stream);  // rule_kernels.cu
 int kernel_mapping_assign(int which, uint32_t worker, int* buf, int cap);
 unsigned long long device_mismatch(const void* a, const void* b, size_t bytes, void* stream);
 float device_max_rel_error(const void* a, const void* b, size_t n, int dtype, void* stream);

@@ -60,9 +60,20 @@ std::string ScheduleConfig::key() const {
 // polling ring slots they did not own, and a missing producer tail -- is fixed
 // in gemm_sm100.cuh, and every point is back.)
 std::vector<ScheduleConfig> schedule_space(const std::string& op_kind) {
+  std::vector<ScheduleConfig> out;
+  if (op_kind == "reduce") {
+    // reduce_template: CTA width of the block-level tree
+    // reduction (one CTA per output element); the rule-based form of short
+    // reductions ignores it
+    for (int t : {128, 256, 512, 64, 32}) {
+      ScheduleConfig c;
+      c.threads_per_block = t;
+      out.push_back(c);
+    }
+    return out;
+  }
   if (op_kind != "matmul" && op_kind != "conv2d" && op_kind != "batch_matmul")
     fail("unknown op kind '", op_kind, "' for schedule_space");
-  std::vector<ScheduleConfig> out;
   // single-SM tiles (128 x N)
   for (int bn : {128, 256, 192, 64, 96})
     for (int sk : {1, 2, 4})

@@ -58,13 +58,13 @@ def test_unsupported_status_code():
     from paper_2210_09603_b200 import Axis, ComputeDAG, TensorNode, load, var, Plan, TaskmapError
     from paper_2210_09603_b200.taskmap import Combiner
     d = ComputeDAG()
-    d.add_input("X", [4, 4])
-    d.nodes.append(TensorNode("Y", [4], kind="reduce", axes=[Axis("i", 4)], reduce_axes=[Axis("j", 4)],
-                              combiner=Combiner.Min, value=load("X", [var("i"), var("j")])))
+    d.add_input("X", [1] * 9)
+    ax = [Axis(f"a{i}", 1) for i in range(9)]
+    d.nodes.append(TensorNode("Y", [1] * 9, kind="compute", axes=ax, value=load("X", [var(a.name) for a in ax])))
     d.outputs = ["Y"]
     with pytest.raises(TaskmapError) as e:
         Plan(d)
-    assert e.value.status == 4  # TM_ERR_UNSUPPORTED: a valid DAG whose anchor is not a sum reduction
+    assert e.value.status == 4  # TM_ERR_UNSUPPORTED: a valid 9-d DAG beyond the rule kernel's 8 axes
 
 
 def test_product_never_imports_oracle():

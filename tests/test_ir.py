@@ -129,9 +129,11 @@ def test_relu_prologue_and_rejected_prologues():
     x = load("X", [var("i"), var("k")])
     k = Plan(dag(relu(x))).describe()["kernels"][0]
     assert k["prologue"] == ["R"] and k["A"].endswith("|> op32(0.000000)")  # RELU
-    with pytest.raises(TaskmapError) as e:
-        Plan(dag(add(x, load("V", [var("i"), var("k")]))))
-    assert e.value.status == 4
+    # a prologue the loader cannot apply (two input elements) is materialised by a
+    # rule-based kernel first; the GEMM then reads it
+    ks = Plan(dag(add(x, load("V", [var("i"), var("k")])))).describe()["kernels"]
+    assert [k["kind"] for k in ks] == ["rule", "gemm"]
+    assert ks[0]["root"] == "R" and ks[1]["prologue"] == [] and ks[1]["A"].startswith("R[")
 
 
 def test_schedule_space_size_and_agnostic():
@@ -143,15 +145,37 @@ def test_schedule_space_size_and_agnostic():
     assert len({(c.block_m, c.block_n, c.split_k, c.pipeline, c.raster, c.grid) for c in s}) == len(s)
 
 
-def test_unsupported_reports_unsupported_status():
+def test_reduce_schedule_space():
+    """SPEC.md:311: schedule_space(op_kind) for op_kind in {matmul, reduce}."""
+    from paper_2210_09603_b200 import schedule_space
+    s = schedule_space("reduce")
+    assert [c.threads_per_block for c in s] == [128, 256, 512, 64, 32]
+
+
+def test_non_matmul_reduction_plans_the_reduce_template():
+    """a max reduction is not a matrix product -> reduce_template."""
     d = ComputeDAG()
     d.add_input("X", [4, 4])
     d.nodes.append(TensorNode("Y", [4], kind="reduce", axes=[Axis("i", 4)], reduce_axes=[Axis("j", 4)],
                               combiner=T.Combiner.Max, value=load("X", [var("i"), var("j")])))
     d.outputs = ["Y"]
-    with pytest.raises(TaskmapError) as e:
-        Plan(d)
-    assert "sum reductions" in str(e.value)
+    (k,) = Plan(d).describe()["kernels"]
+    assert k["kind"] == "reduce" and k["root"] == "Y" and k["reduce"] == 4
+
+
+def test_anchor_free_chain_fuses_into_one_rule_kernel():
+    """the elementwise chain a*2+1 (then ReLU) is one rule-based kernel."""
+    from paper_2210_09603_b200 import relu, add, mul, fimm
+    d = ComputeDAG()
+    d.add_input("A", [1000])
+    d.add_compute("T1", [Axis("i", 1000)], mul(load("A", [var("i")]), fimm(2.0)))
+    d.add_compute("T2", [Axis("i", 1000)], add(load("T1", [var("i")]), fimm(1.0)))
+    d.add_compute("T3", [Axis("i", 1000)], relu(load("T2", [var("i")])))
+    d.outputs = ["T3"]
+    sgs = T.partition(d)
+    assert len(sgs) == 1 and sgs[0]["output"] == "T3" and sgs[0]["prologue"] == ["T1", "T2"]
+    (k,) = Plan(d).describe()["kernels"]
+    assert k["kind"] == "rule" and k["inlined"] == ["T1", "T2"] and "T1" not in k["expr"]
 
 
 def test_workload_flops():
