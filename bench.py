@@ -134,6 +134,10 @@ def build_sweep(torch, device, shard, tuner=None, tune_mode="auto", log=None):
             return default
         cfg, secs, cached = tuner.tune(key, dag, ins, outs, force=(tune_mode == "force"))
         treport["seconds"] += secs
+        # cold tuning time of this workload (enumerate + compile + time + verify over the
+        # whole space), recorded when it was tuned -- now or in the cached entry
+        treport["cold_seconds"] = treport.get("cold_seconds", 0.0) + float(
+            tuner.entries.get(key, {}).get("tuning_time_s", secs) if cached else secs)
         treport["tuned" if not cached else "cached"] += 1
         treport["configs"][key] = cfg_str(cfg)
         if log:
@@ -573,6 +577,7 @@ def main():
                    "tuning": {"mode": args.tune, "workloads_tuned": treport["tuned"],
                               "workloads_cached": treport["cached"],
                               "tuning_time_s": round(treport["seconds"], 2),
+                              "cold_tuning_time_s": round(treport.get("cold_seconds", 0.0), 2),
                               "setup_time_s": round(t_build, 2),
                               "space_size": len(schedule_space("matmul"))}},
         "roofline": roof,

@@ -153,6 +153,12 @@ struct GemmParams {
   int32_t kb_per_split;
   float* workspace;
   int32_t* counters;
+  // one-round grids (every work unit resident): the tile's split_k units wait for
+  // each other's partials and each reduces its own 32-row blocks (lg % split_k ==
+  // ks) instead of the last arriver reducing the whole tile; counters grow
+  // monotonically (arrival a waits for (a / split_k + 1) * split_k)
+  int32_t sk_spin;
+  int32_t sk_pad_;
   int32_t fast_math;  // approximate transcendentals (bf16 outputs)
   int32_t ab_f16;     // 16-bit MMA operands are fp16 (kind::f16 a/b format 0), else bf16 (format 1)
   int32_t out_tma;    // row-major output: stage each 32x16 chunk in smem, TMA-store it

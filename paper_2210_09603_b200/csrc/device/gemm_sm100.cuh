@@ -811,6 +811,83 @@ __device__ __forceinline__ void drain_reduce(const CUtensorMap* tmC, const float
   }
 }
 
+// Split-K final step with the tile's partials staged in shared memory (sk_spin):
+// `stage` holds split_k slabs of this warp's 32 rows x ncols columns, layout
+// [split][col/4][32 lanes] of float4 (slab_f4 float4 each); sums in split order
+// (deterministic), then the same canonical math / staging / TMA store as
+// drain_fast.
+template <int BN, int CG, int OUT_ROW, int ACT, bool RES>
+__device__ __forceinline__ void drain_reduce_smem(const CUtensorMap* tmC, const float4* stage, int split_k,
+                                                  int slab_f4, const float* colbuf, uint8_t* obuf, int ncols,
+                                                  int32_t col_base, int32_t row0, int32_t b, int lane,
+                                                  const uint4* res) {
+  constexpr int GC = OUT_ROW / 2;
+  uint8_t* const orow = obuf + lane * OUT_ROW;
+  const int swz = OUT_ROW == 128 ? (lane & 7) : ((lane >> 1) & 3);
+#pragma unroll 1
+  for (int c = 0; c < ncols; c += 32) {
+    float x[32];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 f = stage[(c / 4 + q) * 32 + lane];
+      x[4 * q] = f.x; x[4 * q + 1] = f.y; x[4 * q + 2] = f.z; x[4 * q + 3] = f.w;
+    }
+#pragma unroll 1
+    for (int sp = 1; sp < split_k; ++sp) {
+      const float4* sl = stage + static_cast<int64_t>(sp) * slab_f4;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 f = sl[(c / 4 + q) * 32 + lane];
+        x[4 * q] += f.x; x[4 * q + 1] += f.y; x[4 * q + 2] += f.z; x[4 * q + 3] += f.w;
+      }
+    }
+    uint4 rq[4];
+    if constexpr (RES) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) rq[q] = __ldg(res + c / 8 + q);
+    }
+    if (c % GC == 0) {
+      if (lane == 0) ptx::bulk_wait_read<0>();
+      __syncwarp();
+    }
+    uint32_t w[16];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 sv = *reinterpret_cast<const float4*>(colbuf + c + 4 * q);
+      const float4 tv = *reinterpret_cast<const float4*>(colbuf + BN + c + 4 * q);
+      float y[4] = {fmaf(x[4 * q], sv.x, tv.x), fmaf(x[4 * q + 1], sv.y, tv.y), fmaf(x[4 * q + 2], sv.z, tv.z),
+                    fmaf(x[4 * q + 3], sv.w, tv.w)};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if constexpr (ACT == 1) y[j] = fmaxf(y[j], 0.f);
+        if constexpr (ACT == 2) y[j] = gelu_tanh_fast(y[j]);
+      }
+      if constexpr (RES) {
+        const uint32_t* rw = reinterpret_cast<const uint32_t*>(rq);
+        const uint32_t w0 = rw[2 * q], w1 = rw[2 * q + 1];
+        y[0] += __uint_as_float(w0 << 16);
+        y[1] += __uint_as_float(w0 & 0xFFFF0000u);
+        y[2] += __uint_as_float(w1 << 16);
+        y[3] += __uint_as_float(w1 & 0xFFFF0000u);
+      }
+      w[2 * q] = pack_bf16x2(y[0], y[1]);
+      w[2 * q + 1] = pack_bf16x2(y[2], y[3]);
+    }
+    const int j0 = (c % GC) / 8;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      *reinterpret_cast<uint4*>(orow + (((j0 + k) ^ swz) << 4)) = make_uint4(w[4 * k], w[4 * k + 1], w[4 * k + 2], w[4 * k + 3]);
+    if ((c + 32) % GC == 0 || c + 32 >= ncols) {
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        ptx::tma_store_3d(tmC, obuf, col_base + (c / GC) * GC, row0, b);
+        ptx::bulk_commit();
+      }
+    }
+  }
+}
+
 // Decodes task `i` of this CTA into (batch, tile_m, tile_n); false once the
 // CTA's task list is exhausted.  Out-of-range tasks are reported via `valid`.
 __device__ __forceinline__ void trace(const GemmParams& p, uint32_t i, int ev, long long t0) {
@@ -879,6 +956,8 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   uint32_t* split_flag = tmem_slot + 1;  // [2], one per epilogue warp group
+  // [8] per epilogue warp: partial slabs bulk-copied into the idle ring (sk_spin)
+  uint64_t* rbar = reinterpret_cast<uint64_t*>(outbuf + Cfg::OUTBUF_BYTES) + 22;
   float* colbuf_all = reinterpret_cast<float*>(outbuf + Cfg::OUTBUF_BYTES + 256);
   uint2* tile_list = reinterpret_cast<uint2*>(reinterpret_cast<uint8_t*>(colbuf_all) + Cfg::COLBUF_BYTES);
 
@@ -898,6 +977,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
       ptx::mbar_init(&full[s], all_tma ? 2 : (p.dbg == 4 ? 4 : 128));
       ptx::mbar_init(&empty[s], 1);
     }
+    for (int w = 0; w < kEpiWarps; ++w) ptx::mbar_init(&rbar[w], 1);
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(&tfull[a], 1);
       // drained by: the group's 4 warps, or all 8 when the groups split columns (of both CTAs)
@@ -1445,8 +1525,12 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
           for (int h = 0; h < 2; ++h) {
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-              float4* dst = reinterpret_cast<float4*>(const_cast<float*>(ws) + ks * static_cast<int64_t>(kBM * BN)) +
-                            (static_cast<int64_t>((cofs + c) / 4 + 4 * h + q) * kBM + rloc);
+              float4* split_base = reinterpret_cast<float4*>(const_cast<float*>(ws) + ks * static_cast<int64_t>(kBM * BN));
+              // sk_spin: per-warp slabs [grp][lg][col/4][32 lanes] (one contiguous block
+              // per 32 rows x half, bulk-copied by the reducer)
+              float4* dst = p.sk_spin
+                                ? split_base + ((grp * 4 + lg) * (kHalf / 4) + (c / 4 + 4 * h + q)) * 32 + lane
+                                : split_base + (static_cast<int64_t>((cofs + c) / 4 + 4 * h + q) * kBM + rloc);
               __stcg(dst, make_float4(__uint_as_float(r[16 * h + 4 * q]), __uint_as_float(r[16 * h + 4 * q + 1]),
                                       __uint_as_float(r[16 * h + 4 * q + 2]), __uint_as_float(r[16 * h + 4 * q + 3])));
             }
@@ -1457,10 +1541,22 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
         __threadfence();
         if (lead) detail::trace(p, i, 9, t0);
         ptx::named_bar_sync(3 + grp, 128);
-        if (gt == 0) split_flag[grp] = (atomicAdd(&p.counters[tile_id * 2 + grp], 1) == p.split_k - 1) ? 1u : 0u;
-        ptx::named_bar_sync(3 + grp, 128);
-        if (lead) detail::trace(p, i, 10, t0);
-        if (*reinterpret_cast<volatile uint32_t*>(&split_flag[grp]) == 0u) continue;
+        if (p.sk_spin) {
+          if (gt == 0) {
+            uint32_t* ctr = reinterpret_cast<uint32_t*>(&p.counters[tile_id * 2 + grp]);
+            const uint32_t sk = static_cast<uint32_t>(p.split_k);
+            const uint32_t target = (atomicAdd(ctr, 1u) / sk + 1u) * sk;
+            while (static_cast<int32_t>(ptx::ld_acquire_u32(ctr) - target) < 0) __nanosleep(64);
+          }
+          ptx::named_bar_sync(3 + grp, 128);
+          if (lead) detail::trace(p, i, 10, t0);
+          if (lg % p.split_k != ks) continue;  // another unit of this tile reduces these rows
+        } else {
+          if (gt == 0) split_flag[grp] = (atomicAdd(&p.counters[tile_id * 2 + grp], 1) == p.split_k - 1) ? 1u : 0u;
+          ptx::named_bar_sync(3 + grp, 128);
+          if (lead) detail::trace(p, i, 10, t0);
+          if (*reinterpret_cast<volatile uint32_t*>(&split_flag[grp]) == 0u) continue;
+        }
         __threadfence();
         const uint4* res = nullptr;
         if (p.canon_res_op >= 0)  // rr is row 0 for rows past M (their stores are clipped)
@@ -1471,6 +1567,38 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
                             ? p.trace + (static_cast<int64_t>(blockIdx.x) * kTraceTiles + i) * kTraceEvents
                             : nullptr;
         if (tk != nullptr && lane == 0) tk[7] = clock64() - t0;  // reduce start (after the fence)
+        if (p.sk_spin) {
+          // the ring is idle (one unit per CTA): this warp's split_k slabs of 32 rows x
+          // the half's columns land there by bulk copies (full bandwidth, no register
+          // round trips), then sum from shared memory
+          const int slab_f4 = (kHalf / 4) * 32;
+          const int reducer = grp * (4 / p.split_k) + lg / p.split_k;
+          float4* stage = reinterpret_cast<float4*>(smA) + static_cast<int64_t>(reducer) * p.split_k * slab_f4;
+          if (lane == 0) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");  // peers' stores -> async-proxy reads
+            const uint32_t slab_b = static_cast<uint32_t>(slab_f4 * 16);
+            ptx::mbar_arrive_expect_tx(&rbar[e], slab_b * static_cast<uint32_t>(p.split_k));
+            for (int sp = 0; sp < p.split_k; ++sp)
+              ptx::bulk_load(stage + static_cast<int64_t>(sp) * slab_f4,
+                             reinterpret_cast<const float4*>(p.workspace + tile_id * p.split_k * static_cast<int64_t>(kBM * BN) +
+                                                             sp * static_cast<int64_t>(kBM * BN)) +
+                                 (grp * 4 + lg) * slab_f4,
+                             slab_b, &rbar[e]);
+          }
+          ptx::mbar_wait(&rbar[e], 0);
+          switch (p.canon_act * 2 + (p.canon_res_op >= 0 ? 1 : 0)) {
+#define TMB_REDS(A, R)                                                                                             \
+  case A * 2 + R:                                                                                                  \
+    detail::drain_reduce_smem<BN, CG, Cfg::OUT_ROW, A, R>(&tmC, stage, p.split_k, slab_f4, colbuf + cofs, obuf,    \
+                                                          hcols, cbase, row0, b, lane, res);                      \
+    break;
+            TMB_REDS(0, 0) TMB_REDS(0, 1) TMB_REDS(1, 0) TMB_REDS(1, 1) TMB_REDS(2, 0) TMB_REDS(2, 1)
+#undef TMB_REDS
+            default: __trap();
+          }
+          if (lead) detail::trace(p, i, 11, t0);
+          continue;
+        }
         switch (p.canon_act * 2 + (p.canon_res_op >= 0 ? 1 : 0)) {
 #define TMB_RED(A, R)                                                                                              \
   case A * 2 + R:                                                                                                  \
@@ -1481,7 +1609,7 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
 #undef TMB_RED
           default: __trap();
         }
-        if (gt == 0) p.counters[tile_id * 2 + grp] = 0;  // self-resetting for the next launch
+        if (gt == 0 && !p.sk_spin) p.counters[tile_id * 2 + grp] = 0;  // self-resetting for the next launch
         if (lead) detail::trace(p, i, 11, t0);
         continue;
       }

@@ -1604,6 +1604,15 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
     int used = grid / k.cg;
     p.tile_map = tile_mapping(int64_t(sp.batch) * p.split_k, p.tiles_m, p.tiles_n, grid / k.cg, plan.cfg.raster, used);
     k.grid = used * k.cg;  // workers of the tile mapping are CTA pairs when cg == 2
+    // split-K reduction spread over the tile's units when they are all resident
+    // (2 or 4 splits: the 8 / split_k reducing warps' slabs, split_k x 32 rows x BN/2
+    // fp32 each, fill 8 * 32 * BN/2 * 4 bytes of the idle ring, which must hold them:
+    // not the 2-stage double-buffer rings of the wide tiles)
+    const int64_t ring_bytes = int64_t(kernel_stages(k)) * (128 + k.bn) * 128;
+    p.sk_spin = (p.split_k > 1 && (p.split_k == 2 || p.split_k == 4) && k.cg == 1 && k.bn % 64 == 0 &&
+                 p.tile_map.tasks == 1 && int64_t(512) * k.bn <= ring_bytes && !std::getenv("TMB_NO_SK_SPIN"))
+                    ? 1
+                    : 0;
     // per-worker task lists, decoded once here instead of in every CTA of every launch
     if (p.tile_map.tasks <= 128 && p.tiles_m < 65536 && p.tiles_n < 65536 && !std::getenv("TMB_NO_TILE_TAB")) {
       const uint32_t workers = p.tile_map.workers, tasks = p.tile_map.tasks;
