@@ -1065,13 +1065,18 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
             continue;
           }
           if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&empty[stage], phase ^ 1u);
-          else ptx::mbar_wait(&empty[stage], phase ^ 1u);
+          // loader warps poll their empty slots instead of parking on them: the ring's
+          // MMA-commit -> refill round trip is what bounds small tiles (measured: ~300
+          // clk per slot with no copies and no MMAs), and a parked warp adds its
+          // wake-up latency to it (-3..4% on the ResNet layers); the MMA warp keeps the
+          // suspending wait (polling it measured no better)
+          else ptx::mbar_wait_poll(&empty[stage], phase ^ 1u);
           uint8_t* a_tile = smA + stage * Cfg::A_BYTES;
           uint8_t* b_tile = smB + stage * Cfg::B_BYTES;
           const int k0 = kb * BK;
           const bool b_stays = p.b_resident && q >= static_cast<uint32_t>(ring);
           if (all_tma) {
-            if (p.dbg == 3) {  // diagnostics: no copies (MMA on stale smem) -> MMA + epilogue floor
+            if (p.dbg == 3 || p.dbg == 7) {  // diagnostics: no copies (MMA on stale smem) -> MMA + epilogue floor
               if (do_a || do_b) {
                 if constexpr (CG == 2) {
                   if (rank == 0) ptx::mbar_arrive(&full[stage]);
@@ -1280,7 +1285,12 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
         const bool own = !all_tma || (2u * q) % R::kLoadWarps == lw || (2u * q + 1u) % R::kLoadWarps == lw;
         if (own) {
           if constexpr (CG == 2) ptx::mbar_wait_acq_cluster(&empty[stage], phase ^ 1u);
-          else ptx::mbar_wait(&empty[stage], phase ^ 1u);
+          // loader warps poll their empty slots instead of parking on them: the ring's
+          // MMA-commit -> refill round trip is what bounds small tiles (measured: ~300
+          // clk per slot with no copies and no MMAs), and a parked warp adds its
+          // wake-up latency to it (-3..4% on the ResNet layers); the MMA warp keeps the
+          // suspending wait (polling it measured no better)
+          else ptx::mbar_wait_poll(&empty[stage], phase ^ 1u);
         }
         if (++stage == ring) { stage = 0; phase ^= 1u; }
       }
@@ -1787,7 +1797,8 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
           if (ptx::elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < Cfg::NSTEP; ++kk) {
-              if (kk > 0 && kk >= ksteps) break;
+              // dbg 6: loads only (no MMA) -> load floor; dbg 7: neither -> ring handshake floor
+              if ((kk > 0 && kk >= ksteps) || p.dbg == 6 || p.dbg == 7) break;
               const uint64_t adesc = ad + static_cast<uint64_t>(kk * a_kstep);
               const uint64_t bdesc = bd + static_cast<uint64_t>(kk * b_kstep);
               const uint32_t accum = (kb != kb0 || kk != 0);
