@@ -52,7 +52,7 @@ typedef struct {
   int32_t block_m, block_n, block_k, warp_m, warp_n, threads_per_block;
   int32_t pipeline, split_k;
   int32_t stages, raster, grid;
-  int32_t math; /* 0 auto, 1 bf16 (tcgen05 kind::f16), 2 tf32 (kind::tf32), 3 fp32 SIMT */
+  int32_t math; /* 0 auto, 1 bf16 (tcgen05 kind::f16), 2 tf32 (kind::tf32), 3 fp32 SIMT, 4 halo conv family */
 } tm_schedule_config;
 
 typedef struct tm_plan tm_plan;       /* compiled fused subgraphs of one DAG */

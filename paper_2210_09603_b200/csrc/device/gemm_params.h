@@ -95,8 +95,10 @@ enum LoaderKind : int32_t {
   LD_IM2COL_G8 = 7,     // same layout and K order as LD_IM2COL_TMA8, gathered by the
                         // 128 loader threads: one 16-byte load per (pixel, tap), the
                         // channels >= C masked to zero (no per-box TMA cost: 49 taps)
-  LD_ROWBAND = 8        // no im2col tile at all: staged input rows read by the MMA through
+  LD_ROWBAND = 8,       // no im2col tile at all: staged input rows read by the MMA through
                         // overlapping no-swizzle descriptors (tm_rowband_kernel)
+  LD_HALO = 9           // same idea for C % 64 == 0: a staged channel-group-major input band
+                        // read by every tap at its own offset (tm_halo_kernel)
 };
 
 // An elementwise prologue op applied to every operand element the gather
@@ -213,6 +215,21 @@ struct GemmParams {
   int32_t rb_bbytes;   // bytes of the packed filter image
   int32_t rb_pad3_;
   const void* rb_bimg; // packed filter smem image [kh][steps][F/8][2][8 rows][16 B]
+  // Halo implicit GEMM (tm_halo_kernel, conv_halo.cuh): stride-1 convs on
+  // channels-last X with C % 64 == 0.  A tile is R output rows of P = Wo + 2 pad
+  // "virtual" pixels (the halo columns compute garbage that is never stored) on
+  // the TMEM lanes; its staged input band [C/8][R + kh - 1 rows][P][8 ch] is read
+  // by every tap's MMA at offset (fh * P + fw) * 16 bytes.
+  int32_t hb_R;        // output rows per tile
+  int32_t hb_P;        // staged pixels per row (Wo + 2 * pad)
+  int32_t hb_rows;     // staged rows per band (R + kh - 1)
+  int32_t hb_G;        // bytes between channel groups in a band (rows * P * 16)
+  int32_t hb_band;     // bytes per band buffer (C/8 groups + read slack, 1 KB aligned)
+  int32_t hb_kb;       // k-blocks per tile: kh * kw * C / 64
+  int32_t hb_tpi;      // tiles per image: ceil(Ho / R)
+  int32_t hb_ftiles;   // F / BN column tiles
+  int32_t hb_total;    // N * tpi * ftiles tiles
+  int32_t hb_stages;   // filter ring depth
   int32_t n_ops;
   int32_t has_mat;  // any SIDE_MAT op
   int32_t out_dtype;

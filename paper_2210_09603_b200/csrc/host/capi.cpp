@@ -81,8 +81,8 @@ ScheduleConfig from_c(const tm_schedule_config* c) {
   s.stages = c->stages;
   s.raster = c->raster;
   s.grid = c->grid;
-  static const char* maths[] = {"auto", "bf16", "tf32", "fp32_simt"};
-  s.math = maths[(c->math >= 0 && c->math <= 3) ? c->math : 0];
+  static const char* maths[] = {"auto", "bf16", "tf32", "fp32_simt", "halo"};
+  s.math = maths[(c->math >= 0 && c->math <= 4) ? c->math : 0];
   if (!s.pipeline) s.stages = 2;
   return s;
 }
@@ -100,7 +100,7 @@ void to_c(const ScheduleConfig& s, tm_schedule_config* c) {
   c->stages = s.stages;
   c->raster = s.raster;
   c->grid = s.grid;
-  c->math = s.math == "bf16" ? 1 : s.math == "tf32" ? 2 : s.math == "fp32_simt" ? 3 : 0;
+  c->math = s.math == "bf16" ? 1 : s.math == "tf32" ? 2 : s.math == "fp32_simt" ? 3 : s.math == "halo" ? 4 : 0;
 }
 }  // namespace
 

@@ -1015,6 +1015,111 @@ bool tma_ok_mnmajor(const Fit& f, const tm_tensor& t, int64_t rows, int64_t k, i
   return (reinterpret_cast<uintptr_t>(t.data) + f.off * es) % 16 == 0;
 }
 
+// Halo implicit GEMM (conv_halo.cuh) for a stride-1 conv anchor with a square
+// odd kernel (pad = (k - 1) / 2, so Ho = H, Wo = W), channels-last bf16/fp16 X
+// with C % 64 == 0, an OHWI (K-major, K order (tap, c)) filter, W + 2 pad <= 128,
+// and a canonical epilogue writing channels-last rows without a residual.
+bool bind_halo(const SubgraphPlan& sp, const std::map<std::string, tm_tensor>& env, BoundKernel& k, Exec& ex,
+               int want_dt, int sms) {
+  GemmParams& p = k.p;
+  if (std::getenv("TMB_NO_HALO")) return false;
+  if (sp.a.kind != OperandPlan::Im2col || sp.b.kind != OperandPlan::ConvFilter || k.simt || k.tf32) return false;
+  if (!p.canon || p.canon_res_op >= 0 || p.out_dtype != want_dt || sp.batch != 1) return false;
+  const ConvInfo& c = sp.a.conv;
+  const tm_tensor& x = lookup(env, c.x_tensor);
+  const tm_tensor& w = lookup(env, sp.b.conv.w_tensor);
+  const int64_t F = sp.N;
+  // (1x1 convs are plain K-major GEMM tiles already: no tap reuse to gain)
+  if (c.stride != 1 || c.kh != c.kw || c.kh < 3 || c.kh % 2 == 0 || c.pad * 2 + 1 != c.kh || c.ho != c.h ||
+      c.wo != c.w)
+    return false;
+  if (x.dtype != want_dt || w.dtype != want_dt || c.c % 64 != 0) return false;
+  // channels-last X (any 16-byte-multiple row / image strides) and OHWI filter rows
+  if (x.stride[1] != 1 || x.stride[3] != c.c || (x.stride[2] * 2) % 16 || (x.stride[0] * 2) % 16 ||
+      reinterpret_cast<uintptr_t>(x.data) % 16)
+    return false;
+  const int64_t K = c.kh * c.kw * c.c;
+  if (w.stride[1] != 1 || w.stride[3] != c.c || w.stride[2] != c.kw * c.c || (w.stride[0] * 2) % 16 ||
+      w.stride[0] < K || reinterpret_cast<uintptr_t>(w.data) % 16)
+    return false;
+  const int P = static_cast<int>(c.w + 2 * c.pad);
+  if (P > 128) return false;
+  const int R = static_cast<int>(std::min<int64_t>(128 / P, c.ho));
+  const int kbs = static_cast<int>(K / 64);
+  if (kbs > 128) return false;
+  const int bn = (F > 64 && F % 128 == 0) ? 128 : 64;
+  if (F % bn) return false;
+  // TMEM lane utilisation: R output rows of Wo valid lanes out of 128 (l4.c2's 7x7
+  // maps keep 49 of 128; the K3 kernel's split-K is faster there)
+  if ((128 / P < c.ho ? 128 / P : c.ho) * c.wo < 96 || c.c / 64 > 8) return false;
+  // output: rows = pixels (n, oh, ow) at a uniform 16-byte-multiple stride, columns contiguous
+  const Addr& oa = p.out_a;
+  if (oa.s_col != 1 || oa.P < sp.M || (oa.s_lo * 2) % 16 || (oa.offset * 2) % 16 ||
+      reinterpret_cast<uintptr_t>(p.out) % 16)
+    return false;
+  const int rows = R + static_cast<int>(c.kh) - 1;
+  const int G = rows * P * 16;
+  // dead TMEM lanes (r >= R * P) read up to (128 + (kh - 1) P + kw) pixels into the
+  // last channel group: slack past the band
+  const int band_bytes = G * static_cast<int>(c.c / 8) + (128 + static_cast<int>(c.kh) * P + static_cast<int>(c.kw)) * 16;
+  // filter stages of nb k-blocks (32 KB where it fits), the deepest ring that fits
+  int nb = 0, stages = 0;
+  for (int cand = bn == 64 ? 4 : 2; cand >= 1 && !stages; cand /= 2)
+    for (int st = 8; st >= 2 && !stages; --st)
+      if (halo_smem(band_bytes, cand * bn * 128, st, bn) <= kMaxSmem) {
+        stages = st;
+        nb = cand;
+      }
+  if (!stages) return false;
+  // tensor maps: the band (5-D, channel-group-major) and the filter ({64, F, K/64})
+  {  // one 64-channel chunk of the band per box: {8 ch, P px, rows, 8 groups, 1 image}
+    const uint64_t dims[5] = {8, (uint64_t)c.w, (uint64_t)c.h, (uint64_t)(c.c / 8), (uint64_t)c.n};
+    const uint64_t strides[4] = {(uint64_t)x.stride[3] * 2, (uint64_t)x.stride[2] * 2, 16, (uint64_t)x.stride[0] * 2};
+    const uint32_t box[5] = {8u, (uint32_t)P, (uint32_t)rows, 8u, 1u};
+    make_tma_2d3d(k.tma_a, x.data, x.dtype, 5, dims, strides, box, 0);
+  }
+  {  // filter {64 c, F, C/64 blocks, taps}: a stage is nb taps of one 64-channel block
+    const uint64_t taps = c.kh * c.kw;
+    const uint64_t dims[4] = {64, (uint64_t)F, (uint64_t)(c.c / 64), taps};
+    const uint64_t strides[3] = {(uint64_t)w.stride[0] * 2, 128, (uint64_t)(c.c / 64) * 128};
+    const uint32_t box[4] = {64u, (uint32_t)bn, 1u, (uint32_t)nb};
+    make_tma_2d3d(k.tma_b, w.data, w.dtype, 4, dims, strides, box, 128);
+  }
+  ConvGeom& g = p.conv;
+  g.n = static_cast<int32_t>(c.n); g.c = static_cast<int32_t>(c.c); g.h = static_cast<int32_t>(c.h);
+  g.w = static_cast<int32_t>(c.w); g.f = static_cast<int32_t>(F); g.kh = static_cast<int32_t>(c.kh);
+  g.kw = static_cast<int32_t>(c.kw); g.stride = 1; g.pad = static_cast<int32_t>(c.pad);
+  g.ho = static_cast<int32_t>(c.ho); g.wo = static_cast<int32_t>(c.wo);
+  p.hb_R = R;
+  p.hb_P = P;
+  p.hb_rows = rows;
+  p.hb_G = G;
+  p.hb_band = band_bytes;
+  p.hb_kb = kbs;
+  p.hb_tpi = static_cast<int32_t>((c.ho + R - 1) / R);
+  p.hb_ftiles = static_cast<int32_t>(F / bn);
+  p.hb_total = static_cast<int32_t>(c.n * p.hb_tpi * p.hb_ftiles);
+  p.hb_stages = stages;
+  p.rb_steps = nb;  // k-blocks per filter stage
+  p.a_loader = LD_HALO;
+  p.b_loader = LD_TMA_K;
+  p.split_k = 1;
+  k.rowband = 2;
+  k.bn = bn;
+  k.cg = 1;
+  k.smem = halo_smem(band_bytes, nb * bn * 128, stages, bn);
+  k.grid = static_cast<int>(std::min<int64_t>(sms, p.hb_total));
+  if (std::getenv("TMB_TRACE")) {
+    void* tr = nullptr;
+    const size_t tb = size_t(k.grid) * kTraceTiles * kTraceEvents * 8;
+    if (cudaMalloc(&tr, tb) != cudaSuccess || cudaMemset(tr, 0, tb) != cudaSuccess)
+      fail_cuda("cudaMalloc failed for the trace buffer");
+    ex.scratch.push_back(tr);
+    p.trace = static_cast<long long*>(tr);
+  }
+  return true;
+}
+
 // Row-band implicit GEMM (conv_rowband.cuh) for a conv anchor whose input
 // pixels are padded to cpad in {4, 8} channels (C <= cpad) with stride * cpad
 // == 8, Wo <= 128, kw + shift <= 8, and a canonical epilogue storing bf16/fp16
@@ -1273,6 +1378,8 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
     // auto: bf16 operands -> tcgen05 kind::f16; fp32 operands keep fp32 semantics on
     // the CUDA-core kernel (matrix operands) or run kind::tf32 (convolutions);
     // tf32 for matrices is an explicit choice (math="tf32")
+    const bool want_halo = math == "halo";  // the halo conv kernel family (bind_halo), else K3
+    if (math == "halo") math = "auto";
     if (math == "auto") {
       if (opa->dtype == TM_F32 || opb->dtype == TM_F32)
         math = (sp.a.kind == OperandPlan::Strided && sp.b.kind == OperandPlan::Strided) ? "fp32_simt" : "tf32";
@@ -1571,7 +1678,7 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       }
     }
     p.fast_math = p.out_dtype != TM_F32;  // approximate tanh only where the output rounding dominates
-    if (bind_rowband(sp, env, k, *ex, want_dt, sms)) {
+    if (bind_rowband(sp, env, k, *ex, want_dt, sms) || (want_halo && bind_halo(sp, env, k, *ex, want_dt, sms))) {
       ex->kernels.push_back(k);
       continue;
     }

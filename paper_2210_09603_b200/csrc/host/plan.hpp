@@ -86,7 +86,7 @@ struct BoundKernel {
   GemmParams p;
   int bn = 128, stages = 4, tf32 = 0, grid = 148, simt = 0, cg = 1;
   int generic = 1;  // 0: compact instantiation (TMA loaders + canonical epilogue only)
-  int rowband = 0;  // 1: tm_rowband_kernel (conv_rowband.cuh); tma_a = staged-row map, smem = its layout
+  int rowband = 0;  // 1: tm_rowband_kernel (conv_rowband.cuh), 2: tm_halo_kernel (conv_halo.cuh); smem = its layout
   int rule = 0;     // 1: rule-based / reduce-template kernel (rule_kernels.cu) running `rj`
   int rule_threads = 128;
   RuleJob rj{};
@@ -113,6 +113,7 @@ void pack_filter(const ConvGeom& g, int kp, void* out, int out_dtype);  // bf16/
 // filter image of the row-band kernel: [kh][steps][bn/8][2][8][8] 16-bit, K order (fw + shift, c < cpad)
 void pack_rowband_filter(const ConvGeom& g, int cpad, int shift, int steps, int bn, void* out, int out_dtype);
 int rowband_smem(int rows, int rowb, int bbytes, int bn);
+int halo_smem(int band_bytes, int stage_bytes, int stages, int bn);
 // storage dtype of materialised intermediates for these inputs: f32 if any input
 // is f32, fp16 if the 16-bit inputs are all fp16, else bf16
 int intermediate_dtype(const tm_tensor* inputs, int n_in);

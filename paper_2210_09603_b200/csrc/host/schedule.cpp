@@ -108,6 +108,14 @@ std::vector<ScheduleConfig> schedule_space(const std::string& op_kind) {
         c.raster = raster;
         out.push_back(c);
       }
+  // conv2d: the halo kernel family (conv_halo.cuh) as one more point; it applies
+  // to stride-1 channels-last convs with C % 64 == 0 and falls back to the
+  // default K3 form elsewhere
+  if (op_kind == "conv2d") {
+    ScheduleConfig c;
+    c.math = "halo";
+    out.push_back(c);
+  }
   return out;
 }
 

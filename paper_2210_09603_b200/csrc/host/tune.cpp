@@ -178,7 +178,12 @@ TuneOutcome tune(const ComputeDAG& d, const tm_tensor* in, int n_in, const tm_te
     return times[times.size() / 2];
   };
 
-  const auto space = schedule_space("matmul");
+  // conv anchors (an im2col operand) tune over the conv2d space (+ the halo family)
+  bool conv = false;
+  const auto plan_default = build_plan(d, ScheduleConfig{}, device);  // (kept alive: the loop reads its kernels)
+  for (const auto& sp : plan_default->kernels)
+    conv = conv || (sp.kind == SubgraphPlan::Gemm && sp.a.kind == OperandPlan::Im2col);
+  const auto space = schedule_space(conv ? "conv2d" : "matmul");
   std::ostringstream rows;
   int best_i = -1, n_correct = 0, n_unsupported = 0;
   std::vector<std::string> failures;

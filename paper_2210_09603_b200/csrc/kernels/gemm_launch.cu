@@ -219,7 +219,8 @@ void launch_bound(const BoundKernel& k, void* stream) {
   } else if (k.rule) {
     launch_rule(k.rj, k.rule_threads, k.grid, stream);
     ok = true;
-  } else if (k.rowband) ok = launch_rowband(k, s);
+  } else if (k.rowband == 2) ok = launch_halo(k, s);
+  else if (k.rowband) ok = launch_rowband(k, s);
   else if (k.cg == 2) ok = launch_cg2(k, s);
   else if (k.tf32) ok = launch_cg1_generic_tf32(k, s);
   else if (!k.generic) ok = launch_cg1_fast(k, s);

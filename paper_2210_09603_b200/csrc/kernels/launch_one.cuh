@@ -73,5 +73,6 @@ bool launch_cg1_generic_tf32(const BoundKernel& k, cudaStream_t s);
 bool launch_cg1_fast(const BoundKernel& k, cudaStream_t s);
 bool launch_cg2(const BoundKernel& k, cudaStream_t s);
 bool launch_rowband(const BoundKernel& k, cudaStream_t s);
+bool launch_halo(const BoundKernel& k, cudaStream_t s);
 
 }  // namespace tmb

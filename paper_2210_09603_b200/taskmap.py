@@ -406,7 +406,7 @@ def reshape_dag(in_shape, out_shape, dtype: DType = DType.F32) -> ComputeDAG:
 
 
 # ----------------------------------------------------------- scheduling --
-_MATH = {"auto": 0, "bf16": 1, "tf32": 2, "fp32_simt": 3}
+_MATH = {"auto": 0, "bf16": 1, "tf32": 2, "fp32_simt": 3, "halo": 4}
 
 
 @dataclass

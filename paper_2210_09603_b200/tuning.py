@@ -38,7 +38,7 @@ class TuningCache:
         if not e or e.get("gate") != GATE_VERSION:
             return None
         c = ScheduleConfig(**e["config"])
-        return c if c in schedule_space("matmul") else None
+        return c if c in schedule_space("conv2d") else None  # conv2d = the matmul space + the halo family
 
     def tune(self, key: str, dag, inputs, outputs, reps: int = 5, force: bool = False):
         """Returns (config, seconds spent tuning now, cached?)."""
