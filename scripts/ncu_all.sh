@@ -19,6 +19,9 @@ cap ffn_gemm1_pair256 tm_gemm 6 python scripts/run_case.py --case ffn --bm 256 -
 cap ffn_gemm2_pair256 tm_gemm 7 python scripts/run_case.py --case ffn --bm 256 --bn 256 --iters 2
 cap attn_qk tm_gemm 3 python scripts/run_case.py --case qk --bn 128 --iters 2
 cap attn_pv tm_gemm 3 python scripts/run_case.py --case pv --bn 64 --iters 2
+cap l1c2_halo halo 3 python scripts/run_case.py --case conv:l1.c2 --math halo --iters 2
+cap l2c2_halo halo 3 python scripts/run_case.py --case conv:l2.c2 --math halo --iters 2
+cap l3c2_halo halo 3 python scripts/run_case.py --case conv:l3.c2 --math halo --iters 2
 cap config1_simt simt 2 python scripts/ncu_cases.py simt
 cap config1_tf32 tm_gemm 2 python scripts/ncu_cases.py tf32
 cap softmax_reduce rule_tree 2 python scripts/ncu_cases.py softmax
@@ -30,6 +33,6 @@ for r in $OUT/*.ncu-rep; do
   ncu -i $r --page details > $OUT/$n.details.txt 2>/dev/null
   python scripts/ncu_lines.py $r 20 > $OUT/$n.lines.txt 2>/dev/null
 done
-mkdir -p $OUT/keep; for k in conv1_rowband l3c2_bn96 ffn_gemm1_pair256; do mv $OUT/$k.ncu-rep $OUT/keep/ 2>/dev/null; done
+mkdir -p $OUT/keep; for k in conv1_rowband l3c2_halo; do mv $OUT/$k.ncu-rep $OUT/keep/ 2>/dev/null; done
 rm -f $OUT/*.ncu-rep
 du -sh $OUT

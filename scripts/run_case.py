@@ -28,12 +28,14 @@ def main():
     ap.add_argument("--sk", type=int, default=1)
     ap.add_argument("--bt", action="store_true", help="store B K-major (transposed)")
     ap.add_argument("--f32out", action="store_true")
+    ap.add_argument("--math", default="auto", help="auto | bf16 | tf32 | fp32_simt | halo")
     ap.add_argument("--trace", action="store_true", help="print the per-tile role timeline of CTA 0/1")
     ap.add_argument("--gap", action="store_true", help="globaltimer gap between two graph-chained launches")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     rnd = lambda s, dt=torch.bfloat16: torch.empty(s, device=dev).uniform_(-1, 1).to(dt)
-    cfg = ScheduleConfig(block_m=a.bm, block_n=a.bn or 128, stages=a.stages, raster=a.raster, grid=a.grid, split_k=a.sk)
+    cfg = ScheduleConfig(block_m=a.bm, block_n=a.bn or 128, stages=a.stages, raster=a.raster, grid=a.grid, split_k=a.sk,
+                         math=a.math)
     if a.case == "ffn":
         T = W.BERT_TOKENS
         cfg.block_n = a.bn or 256
