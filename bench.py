@@ -579,7 +579,8 @@ def main():
                               "tuning_time_s": round(treport["seconds"], 2),
                               "cold_tuning_time_s": round(treport.get("cold_seconds", 0.0), 2),
                               "setup_time_s": round(t_build, 2),
-                              "space_size": len(schedule_space("matmul"))}},
+                              "space_size": len(schedule_space("matmul")),
+                              "conv_space_size": len(schedule_space("conv2d"))}},
         "roofline": roof,
         "breakdown": {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in v.items()}
                       for k, v in groups.items()},
