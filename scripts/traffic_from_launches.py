@@ -19,11 +19,11 @@ def main(src, dst):
     for r in rows[1:]:
         d = per.setdefault(r[ix["ID"]], {"name": r[ix["Kernel Name"]]})
         d[r[ix["Metric Name"]]] = float(r[ix["Metric Value"]].replace(",", ""))
-    launches = [d for d in per.values() if "tm_gemm_kernel" in d["name"] or "tm_rowband_kernel" in d["name"]]
+    launches = [d for d in per.values() if any(k in d["name"] for k in ("tm_gemm_kernel", "tm_rowband_kernel", "tm_halo_kernel"))]
     # sweep order (bench.build_sweep): 53 conv launches, FFN (2), QK^T, PV
     groups = [("conv", 53), ("ffn", 2), ("attn", 2)]
     if len(launches) != sum(n for _, n in groups):
-        raise SystemExit(f"expected 57 tm_gemm / tm_rowband launches (one sweep), got {len(launches)}")
+        raise SystemExit(f"expected 57 tm_gemm / rowband / halo launches (one sweep), got {len(launches)}")
     out, i = {}, 0
     for g, n in groups:
         ls = launches[i:i + n]
