@@ -118,6 +118,10 @@ int32_t tm_exec_num_launches(const tm_exec* e);
 /* Launch geometry of kernel `index`: grid size, CTAs per MMA (1/2), tile N, split-K. */
 tm_status tm_exec_kernel_info(const tm_exec* e, int32_t index, int32_t* grid, int32_t* cta_group,
                               int32_t* block_n, int32_t* split_k, int32_t* a_loader, int32_t* b_loader);
+/* Which kernel family launch `index` runs: TM_KIND_* below. */
+enum { TM_KIND_GEMM = 0, TM_KIND_SIMT = 1, TM_KIND_ROWBAND = 2, TM_KIND_HALO = 3, TM_KIND_RULE_INTERP = 4,
+       TM_KIND_RULE_GENERATED = 5 };
+tm_status tm_exec_kernel_kind(const tm_exec* e, int32_t index, int32_t* kind);
 /* Per-tile role timeline of kernel `index` (exec created with TMB_TRACE=1 in the
  * environment): [grid][64 tiles][16 events] int64 clock64 deltas; see TraceEv. */
 tm_status tm_exec_trace(const tm_exec* e, int32_t index, int64_t* buf, size_t cap);

@@ -22,6 +22,13 @@
 
 namespace tmb {
 
+constexpr int kMaxRuleTensors = 15;  // generated kernels: loaded tensors (+ the output) by pointer
+
+// argument block of a generated (NVRTC) rule kernel (host/rule_codegen.hpp)
+struct RulePtrs {
+  const void* p[kMaxRuleTensors + 1];  // tensors in source order, the output last
+};
+
 enum RuleMode : int32_t { RULE_ELEM = 0, RULE_TREE = 1 };
 
 struct RuleJob {

@@ -342,6 +342,20 @@ tm_status tm_exec_kernel_info(const tm_exec* e, int32_t index, int32_t* grid, in
   });
 }
 
+tm_status tm_exec_kernel_kind(const tm_exec* e, int32_t index, int32_t* kind) {
+  return guarded([&] {
+    if (!e || index < 0 || index >= static_cast<int32_t>(e->e->kernels.size())) fail("bad kernel index");
+    if (!kind) fail("null kind pointer");
+    const auto& k = e->e->kernels[index];
+    *kind = k.rule ? (k.rfn ? TM_KIND_RULE_GENERATED : TM_KIND_RULE_INTERP)
+            : k.simt ? TM_KIND_SIMT
+            : k.rowband == 2 ? TM_KIND_HALO
+            : k.rowband ? TM_KIND_ROWBAND
+                        : TM_KIND_GEMM;
+    return TM_OK;
+  });
+}
+
 tm_status tm_exec_trace(const tm_exec* e, int32_t index, int64_t* buf, size_t cap) {
   return guarded([&] {
     if (!e || index < 0 || index >= static_cast<int32_t>(e->e->kernels.size())) fail("bad kernel index");

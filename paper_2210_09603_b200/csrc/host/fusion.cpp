@@ -17,12 +17,15 @@
 #include <functional>
 #include <mutex>
 #include <cstring>
+#include <cstdlib>
+#include <cstdio>
 #include <random>
 #include <set>
 
 #include "json.hpp"
 #include "plan.hpp"
 #include "dev_eval.hpp"
+#include "rule_codegen.hpp"
 
 namespace tmb {
 
@@ -1301,6 +1304,60 @@ BoundKernel bind_rule(const Plan& plan, const SubgraphPlan& sp, const std::map<s
   k.rule_threads = plan.cfg.threads_per_block > 0 ? plan.cfg.threads_per_block : 128;
   k.grid = sms;  // launch_rule sizes the grid from the SM count
   k.bn = 0;
+  // the generated kernel (NVRTC) unless the expression needs the interpreter,
+  // NVRTC is absent, or TMB_RULE_INTERP=1 forces the bytecode path
+  const char* force = std::getenv("TMB_RULE_INTERP");
+  if (!(force && force[0] == '1')) {
+    RuleSourceSpec spec;
+    spec.expr = sp.rule_expr;
+    spec.vars = vars;
+    for (size_t d = 0; d < n.axes.size(); ++d) spec.ext.push_back(n.axes[d].extent);
+    for (size_t d = 0; d < n.reduce_axes.size(); ++d) spec.red.push_back(n.reduce_axes[d].extent);
+    spec.tensor_names = prog.tensors;
+    spec.tensors = refs;
+    spec.out = j.out;
+    spec.combiner = j.combiner;
+    spec.is_float = j.is_float != 0;
+    rule_launch_shape(j, k.rule_threads, sms, &k.rgrid, &k.rblock);
+    spec.threads = static_cast<int>(k.rblock);
+    spec.mode = tree ? GEN_TREE : GEN_ELEM;
+    int64_t scratch_bytes = 0;
+    if (tree && j.numel < sms && j.red_numel >= 8192) {
+      // fewer outputs than SMs: split each reduction over several CTAs
+      const int64_t by_sm = (8 * int64_t(sms) + j.numel - 1) / j.numel;
+      const int64_t by_len = j.red_numel / (int64_t(k.rblock) * 8);
+      const int64_t S = std::max<int64_t>(2, std::min(by_sm, by_len));
+      spec.mode = GEN_SPLIT;
+      spec.splits = static_cast<int>(S);
+      k.rgrid = static_cast<unsigned>(j.numel * S);
+      scratch_bytes = j.numel * S * 8 + j.numel * 4;
+    } else if (j.n_red > 0 && j.red_numel >= 16 && j.red_numel <= 256) {
+      // short reductions: a lane group per output
+      // (about four loads per lane: independent, unrolled, still whole sectors)
+      int G = 1;
+      while (G * 2 <= 32 && G * 8 <= j.red_numel) G *= 2;
+      spec.mode = GEN_GROUP;
+      spec.group = G;
+      const int64_t want = (j.numel + 256 / G - 1) / (256 / G);
+      k.rgrid = static_cast<unsigned>(std::min<int64_t>(want, int64_t(sms) * 8));
+      k.rblock = 256;
+    }
+    std::string src, why;
+    if (emit_rule_source(spec, src, why)) k.rfn = compile_rule_source(src, why);
+    if (k.rfn) {
+      for (size_t t = 0; t < refs.size(); ++t) k.rp.p[t] = refs[t].ptr;
+      k.rp.p[kMaxRuleTensors] = j.out.ptr;
+      if (scratch_bytes) {
+        void* scratch = nullptr;
+        if (cudaMalloc(&scratch, scratch_bytes) != cudaSuccess || cudaMemset(scratch, 0, scratch_bytes) != cudaSuccess)
+          fail_cuda("cudaMalloc of the split-reduction scratch failed");
+        ex.scratch.push_back(scratch);
+        k.rp.p[refs.size()] = scratch;
+      }
+    } else if (std::getenv("TMB_RULE_VERBOSE")) {
+      std::fprintf(stderr, "[taskmap] rule kernel '%s' keeps the interpreter: %s\n", n.name.c_str(), why.c_str());
+    }
+  }
   return k;
 }
 }  // namespace

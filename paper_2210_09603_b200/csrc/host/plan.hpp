@@ -90,6 +90,9 @@ struct BoundKernel {
   int rule = 0;     // 1: rule-based / reduce-template kernel (rule_kernels.cu) running `rj`
   int rule_threads = 128;
   RuleJob rj{};
+  void* rfn = nullptr;  // generated rule kernel (rule_codegen.hpp); nullptr: the bytecode interpreter runs rj
+  RulePtrs rp{};
+  unsigned rgrid = 0, rblock = 0;
   int smem = 0;
   alignas(64) unsigned char tma_a[128];
   alignas(64) unsigned char tma_b[128];
@@ -119,6 +122,9 @@ int halo_smem(int band_bytes, int stage_bytes, int stages, int bn);
 int intermediate_dtype(const tm_tensor* inputs, int n_in);
 void launch_simt(const BoundKernel& k, void* stream);   // fp32 CUDA-core kernel (simt_fp32.cu)
 void launch_rule(const RuleJob& j, int threads, int sms, void* stream);  // rule_kernels.cu
+// grid and CTA width launch_rule uses for `j` (the generated kernels launch the same shape)
+void rule_launch_shape(const RuleJob& j, int threads, int sms, unsigned* grid, unsigned* block);
+void launch_rule_compiled(void* fn, const RulePtrs& ptrs, unsigned grid, unsigned block, void* stream);
 int kernel_mapping_assign(int which, uint32_t worker, int* buf, int cap);
 unsigned long long device_mismatch(const void* a, const void* b, size_t bytes, void* stream);
 float device_max_rel_error(const void* a, const void* b, size_t n, int dtype, void* stream);

@@ -217,7 +217,8 @@ void launch_bound(const BoundKernel& k, void* stream) {
     launch_simt(k, stream);
     ok = true;
   } else if (k.rule) {
-    launch_rule(k.rj, k.rule_threads, k.grid, stream);
+    if (k.rfn) launch_rule_compiled(k.rfn, k.rp, k.rgrid, k.rblock, stream);
+    else launch_rule(k.rj, k.rule_threads, k.grid, stream);
     ok = true;
   } else if (k.rowband == 2) ok = launch_halo(k, s);
   else if (k.rowband) ok = launch_rowband(k, s);

@@ -245,20 +245,31 @@ __global__ void __launch_bounds__(THREADS) rule_tree_kernel(const RuleJob j) {
 
 }  // namespace
 
-void launch_rule(const RuleJob& j, int threads, int sms, void* stream) {
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+void rule_launch_shape(const RuleJob& j, int threads, int sms, unsigned* grid, unsigned* block) {
   if (j.mode == RULE_TREE) {
     const int64_t g = j.numel < int64_t(sms) * 16 ? j.numel : int64_t(sms) * 16;
-    const unsigned grid = static_cast<unsigned>(g > 0 ? g : 1);
+    *grid = static_cast<unsigned>(g > 0 ? g : 1);
     // CTA width: the largest of 64/128/256/512 not above threads_per_block
-    if (threads >= 512) rule_tree_kernel<512><<<grid, 512, 0, s>>>(j);
-    else if (threads >= 256) rule_tree_kernel<256><<<grid, 256, 0, s>>>(j);
-    else if (threads >= 128) rule_tree_kernel<128><<<grid, 128, 0, s>>>(j);
-    else rule_tree_kernel<64><<<grid, 64, 0, s>>>(j);
+    *block = threads >= 512 ? 512 : threads >= 256 ? 256 : threads >= 128 ? 128 : 64;
   } else {
     const int64_t want = (j.numel + 255) / 256;
     const int64_t g = want < int64_t(sms) * 8 ? want : int64_t(sms) * 8;
-    rule_elem_kernel<<<static_cast<unsigned>(g > 0 ? g : 1), 256, 0, s>>>(j);
+    *grid = static_cast<unsigned>(g > 0 ? g : 1);
+    *block = 256;
+  }
+}
+
+void launch_rule(const RuleJob& j, int threads, int sms, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  unsigned grid, block;
+  rule_launch_shape(j, threads, sms, &grid, &block);
+  if (j.mode == RULE_TREE) {
+    if (block == 512) rule_tree_kernel<512><<<grid, 512, 0, s>>>(j);
+    else if (block == 256) rule_tree_kernel<256><<<grid, 256, 0, s>>>(j);
+    else if (block == 128) rule_tree_kernel<128><<<grid, 128, 0, s>>>(j);
+    else rule_tree_kernel<64><<<grid, 64, 0, s>>>(j);
+  } else {
+    rule_elem_kernel<<<grid, block, 0, s>>>(j);
   }
 }
 

@@ -82,6 +82,7 @@ def load_library():
         "tm_exec_launch": ([P, P], I32),
         "tm_exec_num_launches": ([P], I32),
         "tm_exec_kernel_info": ([P, I32] + [ctypes.POINTER(I32)] * 6, I32),
+        "tm_exec_kernel_kind": ([P, I32, ctypes.POINTER(I32)], I32),
         "tm_exec_trace": ([P, I32, ctypes.POINTER(I64), SZ], I32),
         "tm_plan_launch": ([P, ctypes.POINTER(TmTensor), I32, ctypes.POINTER(TmTensor), I32, P], I32),
         "tm_graph_create": ([ctypes.POINTER(P), I32, I32, ctypes.POINTER(P)], I32),
@@ -490,6 +491,14 @@ class Exec:
         v = [ctypes.c_int32() for _ in range(6)]
         _check(load_library().tm_exec_kernel_info(self._h, index, *[ctypes.byref(x) for x in v]))
         return dict(zip(("grid", "cta_group", "block_n", "split_k", "a_loader", "b_loader"), [x.value for x in v]))
+
+    KERNEL_KINDS = ("gemm", "simt", "rowband", "halo", "rule-interp", "rule-generated")
+
+    def kernel_kind(self, index: int = 0) -> str:
+        """Kernel family of launch `index` (tm_exec_kernel_kind)."""
+        k = ctypes.c_int32()
+        _check(load_library().tm_exec_kernel_kind(self._h, index, ctypes.byref(k)))
+        return self.KERNEL_KINDS[k.value]
 
     def trace(self, index: int = 0):
         """Per-tile role timeline (needs TMB_TRACE=1 at bind time): int64 [grid, 64, 8]."""

@@ -188,3 +188,107 @@ def test_epilogue_beyond_the_register_program_is_cut_into_a_rule_kernel():
     rng = port.Rng(508)
     plan = _check(d, {"A": rng.tensor((m, k), True), "B": rng.tensor((k, n), True)}, {"F": (m, n)}, exact=True)
     assert [k["kind"] for k in plan.describe()["kernels"]] == ["gemm", "rule"]
+
+
+def _bind_run(dag, inputs, out_shapes, cfg=None):
+    import torch
+    outs = {o: torch.full(tuple(out_shapes[o]), float("nan"), dtype=torch.float32, device="cuda") for o in dag.outputs}
+    plan = Plan(dag, cfg or ScheduleConfig())
+    ex = plan.bind([inputs[n] for n in dag.inputs], [outs[o] for o in dag.outputs])
+    ex.launch()
+    torch.cuda.synchronize()
+    kinds = [ex.kernel_kind(i) for i in range(len(plan.describe()["kernels"]))]
+    return {o: outs[o].cpu().numpy() for o in dag.outputs}, kinds
+
+
+def _generated_vs_interpreter(monkeypatch, dag, inputs_np, out_shapes, cfg=None, bitwise=True):
+    """The NVRTC-generated rule kernels against the bytecode interpreter: same
+    promotion rules, no FMA contraction, same reduction order -> bit-identical."""
+    inputs = {k: dev(v, "f32") for k, v in inputs_np.items()}
+    monkeypatch.delenv("TMB_RULE_INTERP", raising=False)
+    gen, kinds_gen = _bind_run(dag, inputs, out_shapes, cfg)
+    monkeypatch.setenv("TMB_RULE_INTERP", "1")
+    ref, kinds_ref = _bind_run(dag, inputs, out_shapes, cfg)
+    monkeypatch.delenv("TMB_RULE_INTERP")
+    for o in dag.outputs:
+        if bitwise:
+            assert np.array_equal(gen[o].view(np.uint32), ref[o].view(np.uint32)), o
+        else:
+            assert port.max_rel_error(gen[o], ref[o]) <= 1e-5, o
+    assert "rule-interp" not in kinds_gen, kinds_gen
+    assert "rule-generated" not in kinds_ref, kinds_ref
+    return kinds_gen
+
+
+def test_generated_softmax_equals_interpreter(monkeypatch):
+    kinds = _generated_vs_interpreter(monkeypatch, _softmax_dag(200, 301),
+                                      {"X": port.Rng(520).tensor((200, 301)) * 4.0}, {"P": (200, 301)})
+    assert kinds == ["rule-generated"] * 4
+
+
+def _row_reduce_dag(rows, n, dtype, combiner=None):
+    d = ComputeDAG()
+    d.add_input("X", [rows, n], dtype)
+    kw = {} if combiner is None else {"combiner": combiner}
+    d.nodes.append(TensorNode("S", [rows], dtype, "reduce", [Axis("o", rows)], [Axis("k", n)],
+                              value=mul(load("X", [var("o"), var("k")]), T.imm(3)), **kw))
+    d.outputs = ["S"]
+    return d
+
+
+@pytest.mark.parametrize("threads", [64, 128, 256, 512])
+@pytest.mark.parametrize("rows,n", [(3, 70001), (1, 1 << 20), (200, 3000), (5000, 48), (777, 17), (20000, 9)])
+def test_generated_reduction_shapes(monkeypatch, threads, rows, n):
+    """Every generated reduction shape -- SPLIT (fewer outputs than SMs, long
+    rows), TREE, GROUP (short rows, many outputs) -- on integer data: int64
+    accumulation makes any association exact, so the generated kernels equal the
+    interpreter bit for bit; Max is order-free on float data as well."""
+    rng = port.Rng(521 + rows)
+    x = rng.tensor((rows, n), True)
+    d = _row_reduce_dag(rows, n, DType.I32)
+    _generated_vs_interpreter(monkeypatch, d, {"X": x}, {"S": (rows,)}, ScheduleConfig(threads_per_block=threads))
+    d = _row_reduce_dag(rows, n, DType.F32, T.Combiner.Max)
+    _generated_vs_interpreter(monkeypatch, d, {"X": rng.tensor((rows, n))}, {"S": (rows,)},
+                              ScheduleConfig(threads_per_block=threads))
+
+
+@pytest.mark.parametrize("rows,n", [(3, 70001), (5000, 48)])
+def test_generated_float_sums_against_the_oracle(rows, n):
+    """Float sums under SPLIT / GROUP associate differently from the interpreter:
+    checked against reference_eval (fp64) with the fp32 tolerance."""
+    d = _row_reduce_dag(rows, n, DType.F32)
+    _check(d, {"X": port.Rng(530 + rows).tensor((rows, n))}, {"S": (rows,)}, exact=False)
+
+
+def test_generated_pooling_integer_and_guards(monkeypatch):
+    """Integer max pool + sum with a padding guard (select on bounds), floor
+    division / modulo in the indices: the integer semantics of the generated code."""
+    n, c, h = 2, 8, 15
+    d = ComputeDAG()
+    d.add_input("X", [n, c, h, h], DType.I32)
+    nn, cc, y, x, r, s = var("n"), var("c"), var("y"), var("x"), var("r"), var("s")
+    ho = (h + 1) // 2
+    iy, ix = sub(add(mul(y, T.imm(2)), r), T.imm(1)), sub(add(mul(x, T.imm(2)), s), T.imm(1))
+    inb = T.land(T.land(T.ge(iy, T.imm(0)), T.lt(iy, T.imm(h))), T.land(T.ge(ix, T.imm(0)), T.lt(ix, T.imm(h))))
+    d.nodes.append(TensorNode("MP", [n, c, ho, ho], DType.I32, "reduce",
+                              [Axis("n", n), Axis("c", c), Axis("y", ho), Axis("x", ho)],
+                              [Axis("r", 3), Axis("s", 3)], combiner=T.Combiner.Max,
+                              value=T.select(inb, load("X", [nn, cc, iy, ix]), T.imm(-1000))))
+    d.add_compute("Q", [Axis("n", n), Axis("c", c), Axis("y", ho), Axis("x", ho)],
+                  add(T.div(load("MP", [nn, cc, y, x]), T.imm(3)), T.mod(load("MP", [nn, cc, y, x]), T.imm(5))),
+                  DType.I32)
+    d.outputs = ["Q"]
+    xv = port.Rng(522).tensor((n, c, h, h), True)
+    kinds = _generated_vs_interpreter(monkeypatch, d, {"X": xv}, {"Q": (n, c, ho, ho)})
+    assert kinds == ["rule-generated", "rule-generated"]
+    _check(d, {"X": xv}, {"Q": (n, c, ho, ho)}, exact=True)
+
+
+def test_generated_rule_kernels_in_the_attention_graph(monkeypatch):
+    b, s, dh = 2, 128, 64
+    d = _attention_dag(b, s, dh, 0.125)
+    rng = port.Rng(523)
+    # the Z sums (128 per row) run as GROUP kernels: float association differs
+    kinds = _generated_vs_interpreter(monkeypatch, d, {n: rng.tensor((b, s, dh)) for n in ("Q", "Kt", "V")},
+                                      {"O": (b, s, dh)}, bitwise=False)
+    assert kinds[1:5] == ["rule-generated"] * 4
