@@ -327,6 +327,70 @@ def config1_lines(torch, device, peak_tf, sm_mhz, reps=50):
 
 
 # -------------------------------------------------------------------- main --
+def chain_line(torch, device, rank, world, args, tuner, timed, stream, dist):
+    """ResNet-50 v1.5 forward as one chain of the product's
+    kernels (53 convs with fused BN / ReLU / residual, max pool, average pool,
+    classifier), activations resident in HBM, replayed as one CUDA graph.  Each
+    rank runs its slice of the 32-image batch; the only exchange is one gather of
+    the logits to rank 0.  e2e adds the H2D of the step's images (pinned host
+    memory) and the D2H of the logits."""
+    from paper_2210_09603_b200.chain import ResNet50Chain
+    from paper_2210_09603_b200.sharding import gather_buffers, gather_to_root, shard_range
+    total = 32 if args.scaling == "strong" else 32 * world
+    sizes = [32] * world if args.scaling == "weak" else [shard_range(32, r, world)[1] - shard_range(32, r, world)[0]
+                                                         for r in range(world)]
+    t0 = time.perf_counter()
+    ch = ResNet50Chain(sizes[rank], 224, device=device, tuner=tuner if args.tune != "off" else None,
+                       force_tune=args.tune == "force")
+    build_s = time.perf_counter() - t0
+    if rank == 0 and ch.tuned:
+        tuner.save()
+    g = torch.Generator(device=device)
+    g.manual_seed(99 + rank)
+    host_img = torch.empty((sizes[rank], 224, 224, 4), dtype=torch.bfloat16)
+    host_img[..., :3] = torch.empty((sizes[rank], 224, 224, 3), device=device).uniform_(-1, 1, generator=g).cpu()
+    host_img = host_img.pin_memory()
+    host_logits = torch.empty(tuple(ch.logits.shape), dtype=ch.logits.dtype).pin_memory()
+    bufs = gather_buffers([ch.logits], 0, [max(sizes)]) if dist is not None else None
+
+    def gather():
+        if dist is not None:
+            gather_to_root([ch.logits], 0, bufs, [sizes])
+
+    def step():
+        ch.replay(stream)
+        gather()
+
+    def e2e():
+        ch.input_buf.copy_(host_img, non_blocking=True)
+        ch.replay(stream)
+        host_logits.copy_(ch.logits, non_blocking=True)
+        gather()
+
+    ch.input_buf.copy_(host_img)
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    ms = timed(step, args.steps)
+    compute_ms = timed(lambda: ch.replay(stream), args.steps)
+    for _ in range(2):
+        e2e()
+    e2e_ms = timed(e2e, args.steps)
+    flops = ch.flops / sizes[rank] * total if sizes[rank] else 0.0
+    return {
+        "workload": "ResNet-50 v1.5 forward chained in HBM (53 implicit-GEMM convs with fused BN/ReLU/residual, "
+                    "max pool, average pool, classifier GEMM), one CUDA graph per rank, one logits gather",
+        "images": total, "per_rank_images": sizes, "ms_per_step": ms, "images_per_s": total / ms * 1e3,
+        "tflops": flops / ms / 1e9, "compute_ms_per_step": compute_ms, "launches_per_rank": ch.num_launches,
+        "gather_bytes_per_rank": ch.logits.numel() * ch.logits.element_size(),
+        "e2e": {"ms_per_step": e2e_ms, "images_per_s": total / e2e_ms * 1e3,
+                "h2d_bytes_per_step": host_img.numel() * host_img.element_size(),
+                "d2h_bytes_per_step": host_logits.numel() * host_logits.element_size()},
+        "tuning": {"tuned": ch.tuned, "cached": ch.cached, "seconds": round(ch.tuning_s, 2),
+                   "build_s": round(build_s, 2)},
+    }
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -337,6 +401,7 @@ def main():
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-config1", action="store_true")
+    ap.add_argument("--no-chain", action="store_true")
     ap.add_argument("--tune", default="auto", choices=["auto", "force", "off"],
                     help="auto: reuse tuning_cache.json entries, tune the rest on the device")
     ap.add_argument("--tuning-cache", default=os.path.join(ROOT, "tuning_cache.json"))
@@ -500,6 +565,10 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = timed(e2e_step, max(2, min(args.steps, 5)))
 
+    chain = None
+    if not args.no_chain:
+        chain = chain_line(torch, device, rank, world, args, tuner, timed, stream, dist)
+
     c1 = None
     if rank == 0 and not args.no_config1:
         c1 = config1_lines(torch, device, peaks()[0], clocks.get("sm_mhz"))
@@ -592,6 +661,7 @@ def main():
         "clocks": clocks,
         "cpu_baseline": cpu,
         "config1": c1,
+        "chain": chain,
     }
     print(json.dumps(out))
     if dist is not None:

@@ -174,6 +174,7 @@ struct GemmParams {
   int32_t canon_t_op;      // op index providing T (-1: constant canon_t)
   int32_t canon_res_slot;  // SIDE_MAT prefetch slot added after the activation (-1: none)
   int32_t canon_res_op;    // op index of that residual (-1: none)
+  int32_t canon_res_pre;   // 1: the residual is added before the activation (act(acc*S+T+R))
   float canon_s, canon_t;
   // optional per-tile role timeline (clock64 relative to CTA start), layout
   // [cta][kTraceTiles][kTraceEvents]; null = tracing off

@@ -500,6 +500,14 @@ __device__ __forceinline__ void apply_canon(const GemmParams& p, float (&v)[16],
     v[4 * q + 2] = fmaf(v[4 * q + 2], s.z, t.z);
     v[4 * q + 3] = fmaf(v[4 * q + 3], s.w, t.w);
   }
+  const bool pre = p.canon_res_pre != 0;
+  if (pre && p.canon_res_slot == 0) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] += mat[0][j];
+  } else if (pre && p.canon_res_slot == 1) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] += mat[1][j];
+  }
   if (p.canon_act == 1) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] = fmaxf(v[j], 0.f);
@@ -512,10 +520,10 @@ __device__ __forceinline__ void apply_canon(const GemmParams& p, float (&v)[16],
       for (int j = 0; j < 16; ++j) v[j] = gelu_precise1(v[j]);
     }
   }
-  if (p.canon_res_slot == 0) {
+  if (!pre && p.canon_res_slot == 0) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] += mat[0][j];
-  } else if (p.canon_res_slot == 1) {
+  } else if (!pre && p.canon_res_slot == 1) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) v[j] += mat[1][j];
   }
@@ -596,6 +604,16 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return d;
 }
 
+// + the bf16 residual elements 4q .. 4q+3 of the 32 (words 2q, 2q+1 of rq[])
+__device__ __forceinline__ void add_res4(float (&x)[4], const uint4 (&rq)[4], int q) {
+  const uint32_t* rw = reinterpret_cast<const uint32_t*>(rq);
+  const uint32_t w0 = rw[2 * q], w1 = rw[2 * q + 1];
+  x[0] += __uint_as_float(w0 << 16);
+  x[1] += __uint_as_float(w0 & 0xFFFF0000u);
+  x[2] += __uint_as_float(w1 << 16);
+  x[3] += __uint_as_float(w1 & 0xFFFF0000u);
+}
+
 #ifdef TMB_FINE_TRACE
 // diagnostics build only (-DTMB_FINE_TRACE): clock64 at each drain step of the
 // first epilogue warp, into trace rows 48.. of the CTA (tracing must be on)
@@ -604,7 +622,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 #define TMB_FT(i) do { } while (0)
 #endif
 
-template <int BN, int CG, int OUT_ROW, int ACT, bool RES>
+template <int BN, int CG, int OUT_ROW, int ACT, int RES>
 __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t taddr, const float* colbuf,
                                            uint8_t* obuf, int ncols, int32_t col_base, int32_t row0,
                                            int32_t b, int lane, const uint4* res, uint64_t* tempty_bar,
@@ -666,19 +684,13 @@ __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t tadd
         w[2 * q + 1] = pack_relu_bf16x2(x[2], x[3]);
         continue;
       }
+      if constexpr (RES == 2) add_res4(x, rq, q);  // act(acc*S + T + R)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if constexpr (ACT == 1) x[j] = fmaxf(x[j], 0.f);
         if constexpr (ACT == 2) x[j] = gelu_tanh_fast(x[j]);
       }
-      if constexpr (RES) {  // bf16 elements 4q .. 4q+3 of the 32: words 2q, 2q+1 of rq[]
-        const uint32_t* rw = reinterpret_cast<const uint32_t*>(rq);
-        const uint32_t w0 = rw[2 * q], w1 = rw[2 * q + 1];
-        x[0] += __uint_as_float(w0 << 16);
-        x[1] += __uint_as_float(w0 & 0xFFFF0000u);
-        x[2] += __uint_as_float(w1 << 16);
-        x[3] += __uint_as_float(w1 & 0xFFFF0000u);
-      }
+      if constexpr (RES == 1) add_res4(x, rq, q);  // act(acc*S + T) + R
       w[2 * q] = pack_bf16x2(x[0], x[1]);
       w[2 * q + 1] = pack_bf16x2(x[2], x[3]);
     }
@@ -723,7 +735,7 @@ __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t tadd
 // and column half from the fp32 workspace (chunk-major [split][col/16][128][16]),
 // all of a 32-column chunk's loads in flight together, then the same canonical
 // math / bf16 staging / TMA store as drain_fast.
-template <int BN, int CG, int OUT_ROW, int ACT, bool RES>
+template <int BN, int CG, int OUT_ROW, int ACT, int RES>
 __device__ __forceinline__ void drain_reduce(const CUtensorMap* tmC, const float* ws, int split_k, int rloc,
                                              int cofs, const float* colbuf, uint8_t* obuf, int ncols,
                                              int32_t col_base, int32_t row0, int32_t b, int lane, const uint4* res,
@@ -779,19 +791,13 @@ __device__ __forceinline__ void drain_reduce(const CUtensorMap* tmC, const float
       const float4 tv = *reinterpret_cast<const float4*>(colbuf + BN + c + 4 * q);
       float y[4] = {fmaf(x[4 * q], sv.x, tv.x), fmaf(x[4 * q + 1], sv.y, tv.y), fmaf(x[4 * q + 2], sv.z, tv.z),
                     fmaf(x[4 * q + 3], sv.w, tv.w)};
+      if constexpr (RES == 2) add_res4(y, rq, q);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if constexpr (ACT == 1) y[j] = fmaxf(y[j], 0.f);
         if constexpr (ACT == 2) y[j] = gelu_tanh_fast(y[j]);
       }
-      if constexpr (RES) {
-        const uint32_t* rw = reinterpret_cast<const uint32_t*>(rq);
-        const uint32_t w0 = rw[2 * q], w1 = rw[2 * q + 1];
-        y[0] += __uint_as_float(w0 << 16);
-        y[1] += __uint_as_float(w0 & 0xFFFF0000u);
-        y[2] += __uint_as_float(w1 << 16);
-        y[3] += __uint_as_float(w1 & 0xFFFF0000u);
-      }
+      if constexpr (RES == 1) add_res4(y, rq, q);
       w[2 * q] = pack_bf16x2(y[0], y[1]);
       w[2 * q + 1] = pack_bf16x2(y[2], y[3]);
     }
@@ -816,7 +822,7 @@ __device__ __forceinline__ void drain_reduce(const CUtensorMap* tmC, const float
 // [split][col/4][32 lanes] of float4 (slab_f4 float4 each); sums in split order
 // (deterministic), then the same canonical math / staging / TMA store as
 // drain_fast.
-template <int BN, int CG, int OUT_ROW, int ACT, bool RES>
+template <int BN, int CG, int OUT_ROW, int ACT, int RES>
 __device__ __forceinline__ void drain_reduce_smem(const CUtensorMap* tmC, const float4* stage, int split_k,
                                                   int slab_f4, const float* colbuf, uint8_t* obuf, int ncols,
                                                   int32_t col_base, int32_t row0, int32_t b, int lane,
@@ -857,19 +863,13 @@ __device__ __forceinline__ void drain_reduce_smem(const CUtensorMap* tmC, const 
       const float4 tv = *reinterpret_cast<const float4*>(colbuf + BN + c + 4 * q);
       float y[4] = {fmaf(x[4 * q], sv.x, tv.x), fmaf(x[4 * q + 1], sv.y, tv.y), fmaf(x[4 * q + 2], sv.z, tv.z),
                     fmaf(x[4 * q + 3], sv.w, tv.w)};
+      if constexpr (RES == 2) add_res4(y, rq, q);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if constexpr (ACT == 1) y[j] = fmaxf(y[j], 0.f);
         if constexpr (ACT == 2) y[j] = gelu_tanh_fast(y[j]);
       }
-      if constexpr (RES) {
-        const uint32_t* rw = reinterpret_cast<const uint32_t*>(rq);
-        const uint32_t w0 = rw[2 * q], w1 = rw[2 * q + 1];
-        y[0] += __uint_as_float(w0 << 16);
-        y[1] += __uint_as_float(w0 & 0xFFFF0000u);
-        y[2] += __uint_as_float(w1 << 16);
-        y[3] += __uint_as_float(w1 & 0xFFFF0000u);
-      }
+      if constexpr (RES == 1) add_res4(y, rq, q);
       w[2 * q] = pack_bf16x2(y[0], y[1]);
       w[2 * q + 1] = pack_bf16x2(y[2], y[3]);
     }
@@ -1596,26 +1596,26 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
                              slab_b, &rbar[e]);
           }
           ptx::mbar_wait(&rbar[e], 0);
-          switch (p.canon_act * 2 + (p.canon_res_op >= 0 ? 1 : 0)) {
+          switch (p.canon_act * 3 + (p.canon_res_op < 0 ? 0 : p.canon_res_pre ? 2 : 1)) {
 #define TMB_REDS(A, R)                                                                                             \
-  case A * 2 + R:                                                                                                  \
+  case A * 3 + R:                                                                                                  \
     detail::drain_reduce_smem<BN, CG, Cfg::OUT_ROW, A, R>(&tmC, stage, p.split_k, slab_f4, colbuf + cofs, obuf,    \
                                                           hcols, cbase, row0, b, lane, res);                      \
     break;
-            TMB_REDS(0, 0) TMB_REDS(0, 1) TMB_REDS(1, 0) TMB_REDS(1, 1) TMB_REDS(2, 0) TMB_REDS(2, 1)
+            TMB_REDS(0, 0) TMB_REDS(0, 1) TMB_REDS(1, 0) TMB_REDS(1, 1) TMB_REDS(1, 2) TMB_REDS(2, 0) TMB_REDS(2, 1)
 #undef TMB_REDS
             default: __trap();
           }
           if (lead) detail::trace(p, i, 11, t0);
           continue;
         }
-        switch (p.canon_act * 2 + (p.canon_res_op >= 0 ? 1 : 0)) {
+        switch (p.canon_act * 3 + (p.canon_res_op < 0 ? 0 : p.canon_res_pre ? 2 : 1)) {
 #define TMB_RED(A, R)                                                                                              \
-  case A * 2 + R:                                                                                                  \
+  case A * 3 + R:                                                                                                  \
     detail::drain_reduce<BN, CG, Cfg::OUT_ROW, A, R>(&tmC, ws, p.split_k, rloc, cofs, colbuf + cofs, obuf, hcols,  \
                                                      cbase, row0, b, lane, res, tk, t0);                           \
     break;
-          TMB_RED(0, 0) TMB_RED(0, 1) TMB_RED(1, 0) TMB_RED(1, 1) TMB_RED(2, 0) TMB_RED(2, 1)
+          TMB_RED(0, 0) TMB_RED(0, 1) TMB_RED(1, 0) TMB_RED(1, 1) TMB_RED(1, 2) TMB_RED(2, 0) TMB_RED(2, 1)
 #undef TMB_RED
           default: __trap();
         }
@@ -1703,13 +1703,13 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
         if (p.trace != nullptr && nvalid <= 4)
           fine = p.trace + (static_cast<int64_t>(blockIdx.x) * kTraceTiles + 48) * kTraceEvents + (nvalid - 1) * 64;
 #endif
-        switch (p.canon_act * 2 + (res != nullptr ? 1 : 0)) {
+        switch (p.canon_act * 3 + (res == nullptr ? 0 : p.canon_res_pre ? 2 : 1)) {
 #define TMB_DRAIN(A, R)                                                                                          \
-  case A * 2 + R:                                                                                                \
+  case A * 3 + R:                                                                                                \
     detail::drain_fast<BN, CG, Cfg::OUT_ROW, A, R>(&tmC, taddr + cofs, colbuf + cofs, obuf, hcols, cb, row0, b,  \
                                                    lane, res, &tempty[abuf], fine, drow, dcols);                 \
     break;
-          TMB_DRAIN(0, 0) TMB_DRAIN(0, 1) TMB_DRAIN(1, 0) TMB_DRAIN(1, 1) TMB_DRAIN(2, 0) TMB_DRAIN(2, 1)
+          TMB_DRAIN(0, 0) TMB_DRAIN(0, 1) TMB_DRAIN(1, 0) TMB_DRAIN(1, 1) TMB_DRAIN(1, 2) TMB_DRAIN(2, 0) TMB_DRAIN(2, 1)
 #undef TMB_DRAIN
           default: __trap();
         }

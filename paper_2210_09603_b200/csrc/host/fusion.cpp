@@ -1668,16 +1668,32 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       p.canon_s = 1.f;
       p.canon_t = 0.f;
       p.canon_s_op = p.canon_t_op = p.canon_res_slot = p.canon_res_op = -1;
+      p.canon_res_pre = 0;
       auto is = [&](int kind) { return i < n && p.ops[i].kind == kind; };
       if (is(EPI_MUL_C)) { p.canon_s = p.ops[i].c; ++i; }
       else if (is(EPI_MUL_T) && p.ops[i].side == SIDE_COL) { p.canon_s_op = i; ++i; }
       if (is(EPI_ADD_C)) { p.canon_t = p.ops[i].c * (p.canon_s_op < 0 ? 1.f : 1.f); ++i; }
       else if (is(EPI_SUB_C)) { p.canon_t = -p.ops[i].c; ++i; }
       else if (is(EPI_ADD_T) && p.ops[i].side == SIDE_COL) { p.canon_t_op = i; ++i; }
+      // residual before the activation (ResNet's relu(bn(conv) + identity)) or after it
+      if (is(EPI_ADD_T) && p.ops[i].side == SIDE_MAT) {
+        p.canon_res_slot = p.ops[i].slot;
+        p.canon_res_op = i;
+        p.canon_res_pre = 1;
+        ++i;
+      }
       if (is(EPI_RELU)) { p.canon_act = 1; ++i; }
       else if (is(EPI_GELU_TANH)) { p.canon_act = 2; ++i; }
-      if (is(EPI_ADD_T) && p.ops[i].side == SIDE_MAT) { p.canon_res_slot = p.ops[i].slot; p.canon_res_op = i; ++i; }
-      p.canon = (i == n && !std::getenv("TMB_NO_CANON")) ? 1 : 0;
+      if (p.canon_res_op < 0 && is(EPI_ADD_T) && p.ops[i].side == SIDE_MAT) {
+        p.canon_res_slot = p.ops[i].slot;
+        p.canon_res_op = i;
+        ++i;
+      }
+      // a residual before "no activation" is the same sum as after it; GELU(x + R)
+      // is left to the generic epilogue (the compact drains instantiate ReLU only)
+      if (p.canon_res_pre && p.canon_act == 0) p.canon_res_pre = 0;
+      const bool pre_ok = !p.canon_res_pre || p.canon_act == 1;
+      p.canon = (i == n && pre_ok && !std::getenv("TMB_NO_CANON")) ? 1 : 0;
     }
     {
       const tm_tensor& t = lookup(env, sp.out.tensor);

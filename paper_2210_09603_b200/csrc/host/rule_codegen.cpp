@@ -11,6 +11,7 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <algorithm>
 #include <cinttypes>
 #include <cstdio>
 #include <cstring>
@@ -212,19 +213,21 @@ __device__ __forceinline__ i64 ifloordiv(i64 a, i64 b) {
 __device__ __forceinline__ i64 ifloormod(i64 a, i64 b) { return b == 0 ? 0 : a - ifloordiv(a, b) * b; }
 )";
 
-// row-major decomposition of `flat` into v[first..first+ext.size())
-void decompose(std::ostringstream& o, const char* flat, const std::vector<int64_t>& ext, int first, const char* ind) {
+// decomposition of `flat` over `dims` = (variable slot, extent), outermost
+// first: the last entry varies fastest
+void decompose(std::ostringstream& o, const char* flat, const std::vector<std::pair<int, int64_t>>& dims,
+               const char* ind) {
   // 32-bit division by the literal extents when the domain fits (mul-hi sequences)
   int64_t total = 1;
-  for (auto e : ext) total *= e;
+  for (const auto& d : dims) total *= d.second;
   const bool narrow = total < (int64_t(1) << 31);
   o << ind << "{\n" << ind << "  " << (narrow ? "unsigned rem = (unsigned)" : "i64 rem = ") << flat << ";\n";
-  for (int d = static_cast<int>(ext.size()) - 1; d >= 0; --d) {
+  for (int d = static_cast<int>(dims.size()) - 1; d >= 0; --d) {
     if (d == 0) {
-      o << ind << "  v" << first + d << " = rem;\n";
+      o << ind << "  v" << dims[d].first << " = rem;\n";
     } else {
-      o << ind << "  v" << first + d << " = rem % " << ext[d] << (narrow ? "u" : "LL") << "; rem /= " << ext[d]
-        << (narrow ? "u" : "LL") << ";\n";
+      o << ind << "  v" << dims[d].first << " = rem % " << dims[d].second << (narrow ? "u" : "LL") << "; rem /= "
+        << dims[d].second << (narrow ? "u" : "LL") << ";\n";
     }
   }
   o << ind << "}\n";
@@ -281,12 +284,24 @@ bool emit_rule_source(const RuleSourceSpec& s, std::string& src, std::string& wh
   for (int i = 0; i < nsp + nred; ++i) alias << "#define v" << i << " v[" << i << "]\n";
   o << alias.str();
   const std::string valc = af && !vf ? as_f(val, false) : val;
+  // outputs are visited in the output tensor's memory order (axes by decreasing
+  // stride), so consecutive threads store -- and, for same-layout inputs such as
+  // channels-last pooling, load -- consecutive addresses; values do not depend
+  // on the visiting order
+  std::vector<std::pair<int, int64_t>> sp_dims, red_dims;
+  for (int d = 0; d < nsp; ++d) sp_dims.push_back({d, s.ext[d]});
+  std::stable_sort(sp_dims.begin(), sp_dims.end(), [&](const auto& a, const auto& b) {
+    const int64_t sa = s.out.stride[a.first] < 0 ? -s.out.stride[a.first] : s.out.stride[a.first];
+    const int64_t sb = s.out.stride[b.first] < 0 ? -s.out.stride[b.first] : s.out.stride[b.first];
+    return sa > sb;
+  });
+  for (int d = 0; d < nred; ++d) red_dims.push_back({nsp + d, s.red[d]});
   if (s.mode == GEN_ELEM) {
     o << "extern \"C\" __global__ void __launch_bounds__(256) tmb_rule(const Ptrs P) {\n"
       << "  const i64 step = (i64)gridDim.x * 256;\n"
       << "  for (i64 flat = (i64)blockIdx.x * 256 + threadIdx.x; flat < " << numel << "LL; flat += step) {\n"
       << "    " << vdecl << "\n";
-    decompose(o, "flat", s.ext, 0, "    ");
+    decompose(o, "flat", sp_dims, "    ");
     if (nred == 0) {
       o << "    const float x = " << as_f(val, vf) << ";\n";
     } else {
@@ -311,10 +326,10 @@ bool emit_rule_source(const RuleSourceSpec& s, std::string& src, std::string& wh
       << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
       << "  for (i64 o = blockIdx.x; o < " << numel << "LL; o += gridDim.x) {\n"
       << "    " << vdecl << "\n";
-    decompose(o, "o", s.ext, 0, "    ");
+    decompose(o, "o", sp_dims, "    ");
     o << "    " << at << " acc = " << ident << ";\n"
       << "#pragma unroll 4\n    for (i64 r = threadIdx.x; r < " << red_numel << "LL; r += " << T << ") {\n";
-    decompose(o, "r", s.red, nsp, "      ");
+    decompose(o, "r", red_dims, "      ");
     o << "      acc = comb(acc, " << valc << ");\n"
       << "    }\n"
       << "#pragma unroll\n    for (int sft = 16; sft >= 1; sft >>= 1) acc = comb(acc, __shfl_xor_sync(0xffffffffu, acc, sft));\n"
@@ -333,9 +348,9 @@ bool emit_rule_source(const RuleSourceSpec& s, std::string& src, std::string& wh
       << "    " << vdecl << "\n"
       << "    " << at << " acc = " << ident << ";\n"
       << "    if (o < " << numel << "LL) {\n";
-    decompose(o, "o", s.ext, 0, "      ");
+    decompose(o, "o", sp_dims, "      ");
     o << "#pragma unroll 4\n      for (i64 r = g; r < " << red_numel << "LL; r += " << G << ") {\n";
-    decompose(o, "r", s.red, nsp, "        ");
+    decompose(o, "r", red_dims, "        ");
     o << "        acc = comb(acc, " << valc << ");\n      }\n    }\n";
     if (G > 1)
       o << "#pragma unroll\n    for (int sft = " << G / 2
@@ -354,13 +369,13 @@ bool emit_rule_source(const RuleSourceSpec& s, std::string& src, std::string& wh
       << "  const i64 o = blockIdx.x / " << S << ";\n"
       << "  const int sidx = blockIdx.x % " << S << ";\n"
       << "  " << vdecl << "\n";
-    decompose(o, "o", s.ext, 0, "  ");
+    decompose(o, "o", sp_dims, "  ");
     o << "  " << at << " acc = " << ident << ";\n"
       << "  const i64 lo = (i64)sidx * " << chunk << "LL;\n"
       << "  const i64 hi = lo + " << chunk << "LL < " << red_numel << "LL ? lo + " << chunk << "LL : " << red_numel
       << "LL;\n"
       << "#pragma unroll 4\n  for (i64 r = lo + threadIdx.x; r < hi; r += " << T << ") {\n";
-    decompose(o, "r", s.red, nsp, "    ");
+    decompose(o, "r", red_dims, "    ");
     o << "    acc = comb(acc, " << valc << ");\n  }\n"
       << "#pragma unroll\n  for (int sft = 16; sft >= 1; sft >>= 1) acc = comb(acc, __shfl_xor_sync(0xffffffffu, acc, sft));\n"
       << "  if (lane == 0) sh[warp] = acc;\n  __syncthreads();\n"

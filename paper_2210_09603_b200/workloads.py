@@ -135,3 +135,120 @@ def matmul_bias_relu_dag(m: int, n: int, k: int, dtype: DType = DType.F32) -> Co
                                                                load("Bias", [var("j")]))), dtype)
     d.outputs = ["D"]
     return d
+
+
+# ---------------------------------------------------------------- network chain --
+# ResNet-50 v1.5 as one chain of the tensor programs above:
+# stem conv + max pool, 16 bottleneck blocks (1x1 -> 3x3 (stride) -> 1x1 with the
+# residual add fused into the last conv's epilogue, downsample conv on the first
+# block of each stage), global average pool, classifier GEMM.
+
+def conv_bn_dag(layer: ConvLayer, batch: int, relu_out: bool = True, residual: bool = False,
+                dtype: DType = DType.F32) -> ComputeDAG:
+    """Z = [relu](conv(X, W) * Scale[p] + Shift[p] [+ R[n,p,oh,ow]]) -- the bottleneck's
+    conv kinds: c1/c2 (ReLU), c3 (residual, then ReLU), downsample (neither)."""
+    d = conv2d_im2col_dag(batch, layer.c, layer.h, layer.h, layer.f, layer.k, layer.k, layer.s, layer.p, dtype)
+    out = d.at("Out")
+    d.add_input("Scale", [layer.f], dtype)
+    d.add_input("Shift", [layer.f], dtype)
+    idx = [var("n"), var("p"), var("oh"), var("ow")]
+    v = add(mul(load("Out", idx), load("Scale", [var("p")])), load("Shift", [var("p")]))
+    if residual:
+        ho = layer.out_hw()
+        d.add_input("R", [batch, layer.f, ho, ho], dtype)
+        v = add(v, load("R", idx))
+    d.add_compute("Z", [Axis(a.name, a.extent) for a in out.axes], relu(v) if relu_out else v, dtype)
+    d.outputs = ["Z"]
+    return d
+
+
+def maxpool_dag(batch: int, c: int, h: int, k: int = 3, s: int = 2, p: int = 1,
+                dtype: DType = DType.F32) -> ComputeDAG:
+    """Y[n,c,y,x] = max over the k x k window at (y*s - p, x*s - p); out-of-image taps
+    are excluded by a guard (reduce_template with the Max combiner)."""
+    from .taskmap import Combiner, ge, land, lt, select, sub
+    from .taskmap import imm as iimm
+    ho = (h + 2 * p - k) // s + 1
+    d = ComputeDAG()
+    d.add_input("X", [batch, c, h, h], dtype)
+    nn, cc, y, x, r, q = var("n"), var("c"), var("y"), var("x"), var("r"), var("q")
+    iy = sub(add(mul(y, iimm(s)), r), iimm(p))
+    ix = sub(add(mul(x, iimm(s)), q), iimm(p))
+    inb = land(land(ge(iy, iimm(0)), lt(iy, iimm(h))), land(ge(ix, iimm(0)), lt(ix, iimm(h))))
+    d.nodes.append(TensorNode("Y", [batch, c, ho, ho], dtype, "reduce",
+                              [Axis("n", batch), Axis("c", c), Axis("y", ho), Axis("x", ho)],
+                              [Axis("r", k), Axis("q", k)], combiner=Combiner.Max,
+                              value=select(inb, load("X", [nn, cc, iy, ix]), fimm(-3.0e38))))
+    d.outputs = ["Y"]
+    return d
+
+
+def avgpool_dag(batch: int, c: int, h: int, dtype: DType = DType.F32) -> ComputeDAG:
+    """G[n,c] = mean over the h x h map (a sum reduction of X / h^2)."""
+    d = ComputeDAG()
+    d.add_input("X", [batch, c, h, h], dtype)
+    d.nodes.append(TensorNode("G", [batch, c], dtype, "reduce", [Axis("n", batch), Axis("c", c)],
+                              [Axis("y", h), Axis("x", h)],
+                              value=mul(load("X", [var("n"), var("c"), var("y"), var("x")]), fimm(1.0 / (h * h)))))
+    d.outputs = ["G"]
+    return d
+
+
+def linear_dag(m: int, n: int, k: int, dtype: DType = DType.F32) -> ComputeDAG:
+    """Y = A B + Bias (the classifier)."""
+    d = matmul_dag(m, n, k, dtype)
+    d.add_input("Bias", [n], dtype)
+    d.add_compute("D", [Axis("i", m), Axis("j", n)], add(load("C", [var("i"), var("j")]), load("Bias", [var("j")])),
+                  dtype)
+    d.outputs = ["D"]
+    return d
+
+
+@dataclass(frozen=True)
+class ChainStage:
+    """One kernel group of the network chain: `kind` in conv / maxpool / avgpool /
+    linear; `src` / `res` name the activations it reads, `dst` the one it writes;
+    `layer` is the RESNET50 table entry whose tuned schedule a conv reuses."""
+    kind: str
+    dst: str
+    src: str
+    res: str = ""
+    conv: ConvLayer = None
+    layer: str = ""
+    relu: bool = True
+
+
+def resnet50_stages(image: int = 224, classes: int = 1000, blocks=(3, 4, 6, 3)) -> List[ChainStage]:
+    """The chain's stages in execution order.  At image 224 every conv equals the
+    RESNET50 table entry named in `layer` (same shape; its tuned schedule applies)."""
+    st = []
+    h = image
+    stem = ConvLayer("conv1", 3, h, 64, 7, 2, 3, 1)
+    st.append(ChainStage("conv", "stem", "input", conv=stem, layer="conv1"))
+    h = stem.out_hw()
+    st.append(ChainStage("maxpool", "pool", "stem"))
+    h = (h + 2 - 3) // 2 + 1
+    cin, cur = 64, "pool"
+    for li, (nb, width) in enumerate(zip(blocks, (64, 128, 256, 512))):
+        for b in range(nb):
+            first = b == 0
+            s = 2 if first and li > 0 else 1
+            pre = f"l{li + 1}.b{b}"
+            c1 = ConvLayer(f"{pre}.c1", cin, h, width, 1, 1, 0, 1)
+            c1_tab = "l1.c1a" if (li == 0 and first) else (f"l{li + 1}.c1a" if first else f"l{li + 1}.c1")
+            st.append(ChainStage("conv", f"{pre}.c1", cur, conv=c1, layer=c1_tab))
+            c2 = ConvLayer(f"{pre}.c2", width, h, width, 3, s, 1, 1)
+            st.append(ChainStage("conv", f"{pre}.c2", f"{pre}.c1", conv=c2,
+                                 layer=f"l{li + 1}.c2s" if s == 2 else f"l{li + 1}.c2"))
+            ho = c2.out_hw()
+            res = cur
+            if first:
+                ds = ConvLayer(f"{pre}.ds", cin, h, width * 4, 1, s, 0, 1)
+                st.append(ChainStage("conv", f"{pre}.ds", cur, conv=ds, layer=f"l{li + 1}.ds", relu=False))
+                res = f"{pre}.ds"
+            c3 = ConvLayer(f"{pre}.c3", width, ho, width * 4, 1, 1, 0, 1)
+            st.append(ChainStage("conv", f"{pre}.c3", f"{pre}.c2", res=res, conv=c3, layer=f"l{li + 1}.c3"))
+            cur, cin, h = f"{pre}.c3", width * 4, ho
+    st.append(ChainStage("avgpool", "gap", cur))
+    st.append(ChainStage("linear", "logits", "gap"))
+    return st
