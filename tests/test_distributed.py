@@ -108,3 +108,60 @@ def test_plan_device_follows_the_process_gpu():
     assert _resolve_device(2) == 2
     assert _resolve_device(None, [object(), FakeCuda()]) == 5
     assert isinstance(_resolve_device(None), int)
+
+
+class _FakeChain:
+    """Stands in for chain.ResNet50Chain (GPU-only) on CPU: per-image logits from
+    the rank's slice of the images, so the sharded result is checkable."""
+
+    def __init__(self, batch, image, configs=None, seed=0):
+        g = torch.Generator().manual_seed(seed)
+        self.w = torch.randn(3, 10, generator=g)  # weights identical on every rank
+        self.x = torch.zeros(batch, 3, image, image)
+        self.logits = torch.zeros(batch, 10)
+
+    def set_input(self, images):
+        self.x.copy_(images)
+
+    def replay(self):
+        self.logits.copy_(self.x.mean(dim=(2, 3)) @ self.w)
+        return self.logits
+
+
+def _chain_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2210_09603_b200 import chain as C
+        C.ResNet50Chain = _FakeChain
+        imgs = torch.randn(7, 3, 5, 5, generator=torch.Generator().manual_seed(3))
+        ch, logits = C.run_sharded(7, rank, world, image=5, images=imgs, seed=1)
+        a, b = shard_range(7, rank, world)
+        assert ch.logits.shape[0] == b - a
+        if rank == 0:
+            want = _FakeChain(7, 5, seed=1)
+            want.set_input(imgs)
+            q.put(bool(torch.allclose(logits, want.replay(), rtol=1e-6, atol=1e-6)))
+        else:
+            assert logits is None
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(180)
+@pytest.mark.parametrize("world", [2, 3])
+def test_gloo_chain_level_sharding(world):
+    """Row f2: each rank runs the whole chain on its slice of the batch (7 images,
+    uneven shards) and the logits are gathered once; the result equals the
+    unsharded chain."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_chain_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(150)
+    assert all(p.exitcode == 0 for p in procs)
+    assert q.get(timeout=5) is True
