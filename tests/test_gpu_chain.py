@@ -117,3 +117,28 @@ def test_full_size_chain_batch32():
     want = chain_ref(c)["logits"]
     assert _rel(c.logits, want) <= 5e-2, _rel(c.logits, want)
     assert c.flops > 1.3e11  # 4.1 GFLOP per image
+
+
+@pytest.mark.parametrize("split_k", [1, 2, 4])
+def test_residual_before_relu_compact_drain_exact(split_k):
+    """The chain's c3 epilogue relu(acc*S + T + R) on the compact (TMA-fed,
+    TMA-stored) kernel: channels-last bf16 in and out, integer data -> the fp32
+    value is exact and the bf16 store rounds it like round_bf16 (plain drain and
+    the split-K reductions)."""
+    import torch
+    from paper_2210_09603_b200 import Plan, ScheduleConfig
+    _need_ref()
+    L = W.ConvLayer("t", 64, 14, 256, 1, 1, 0, 1)
+    d = W.conv_bn_dag(L, 2, residual=True)
+    rng = port.Rng(610 + split_k)
+    ins = {"X": rng.tensor((2, 64, 14, 14), True), "W": rng.tensor((256, 64, 1, 1), True),
+           "Scale": rng.tensor((256,), True), "Shift": rng.tensor((256,), True),
+           "R": rng.tensor((2, 256, 14, 14), True)}
+    t = {k: dev(v, "bf16", "cl" if v.ndim == 4 else None) for k, v in ins.items()}
+    z = torch.empty((2, 256, 14, 14), device="cuda", dtype=torch.bfloat16).contiguous(memory_format=torch.channels_last)
+    ex = Plan(d, ScheduleConfig(block_n=256, split_k=split_k)).bind([t[n] for n in d.inputs], [z])
+    ex.launch()
+    torch.cuda.synchronize()
+    want = port.round_bf16(oracle_eval(d, ins, {"Z": (2, 256, 14, 14)})["Z"])
+    assert np.array_equal(z.float().cpu().numpy(), want)
+    assert ex.kernel_kind(0) == "gemm"
