@@ -31,7 +31,7 @@ struct Unsupported {
 
 std::string hex_i64(int64_t v) {
   char b[40];
-  std::snprintf(b, sizeof b, "((i64)0x%016" PRIx64 "ULL)", static_cast<uint64_t>(v));
+  std::snprintf(b, sizeof b, "((ix)0x%016" PRIx64 "ULL)", static_cast<uint64_t>(v));
   return b;
 }
 std::string f32_lit(double v) {
@@ -66,10 +66,10 @@ struct Gen {
     if (static_cast<int>(rank) != r.rank) throw Unsupported{"load rank differs from the bound tensor"};
     const int h = n_helpers++;
     helpers << "__device__ __forceinline__ float ld" << h << "(const Ptrs& P";
-    for (size_t d = 0; d < rank; ++d) helpers << ", i64 x" << d;
+    for (size_t d = 0; d < rank; ++d) helpers << ", ix x" << d;
     helpers << ") {\n  if (!(true";
-    for (size_t d = 0; d < rank; ++d) helpers << " && x" << d << " >= 0 && x" << d << " < " << r.shape[d] << "LL";
-    helpers << ")) return __int_as_float(0x7fffffff);\n  const i64 off = 0";
+    for (size_t d = 0; d < rank; ++d) helpers << " && x" << d << " >= 0 && x" << d << " < " << r.shape[d];
+    helpers << ")) return __int_as_float(0x7fffffff);\n  const ix off = 0";
     for (size_t d = 0; d < rank; ++d) helpers << " + x" << d << " * " << hex_i64(r.stride[d]);
     helpers << ";\n  const " << elem_type(r.store) << "* p = (const " << elem_type(r.store) << "*)P.p[" << t << "];\n";
     if (r.store == ev::ST_F32) helpers << "  return __ldg(p + off);\n";
@@ -81,10 +81,10 @@ struct Gen {
 
   std::string table_helper(const std::vector<int64_t>& tab) {
     const int h = n_helpers++;
-    helpers << "__device__ const i64 tab" << h << "[" << (tab.empty() ? 1 : tab.size()) << "] = {";
+    helpers << "__device__ const ix tab" << h << "[" << (tab.empty() ? 1 : tab.size()) << "] = {";
     for (size_t i = 0; i < tab.size(); ++i) helpers << (i ? ", " : "") << hex_i64(tab[i]);
     if (tab.empty()) helpers << "0";
-    helpers << "};\n__device__ __forceinline__ i64 lut" << h << "(i64 x) { return (x < 0 || x >= " << tab.size()
+    helpers << "};\n__device__ __forceinline__ ix lut" << h << "(ix x) { return (x < 0 || x >= " << tab.size()
             << "LL) ? 0 : tab" << h << "[x]; }\n";
     return "lut" + std::to_string(h);
   }
@@ -120,14 +120,14 @@ struct Gen {
           }
           isf = false;
           switch (e->bop) {
-            case BinOp::And: return "((i64)((" + x + " != 0.f) & (" + y + " != 0.f)))";
-            case BinOp::Or: return "((i64)((" + x + " != 0.f) | (" + y + " != 0.f)))";
-            case BinOp::Lt: return "((i64)(" + x + " < " + y + "))";
-            case BinOp::Le: return "((i64)(" + x + " <= " + y + "))";
-            case BinOp::Gt: return "((i64)(" + x + " > " + y + "))";
-            case BinOp::Ge: return "((i64)(" + x + " >= " + y + "))";
-            case BinOp::Eq: return "((i64)(" + x + " == " + y + "))";
-            default: return "((i64)(" + x + " != " + y + "))";
+            case BinOp::And: return "((ix)((" + x + " != 0.f) & (" + y + " != 0.f)))";
+            case BinOp::Or: return "((ix)((" + x + " != 0.f) | (" + y + " != 0.f)))";
+            case BinOp::Lt: return "((ix)(" + x + " < " + y + "))";
+            case BinOp::Le: return "((ix)(" + x + " <= " + y + "))";
+            case BinOp::Gt: return "((ix)(" + x + " > " + y + "))";
+            case BinOp::Ge: return "((ix)(" + x + " >= " + y + "))";
+            case BinOp::Eq: return "((ix)(" + x + " == " + y + "))";
+            default: return "((ix)(" + x + " != " + y + "))";
           }
         }
         isf = false;
@@ -139,14 +139,14 @@ struct Gen {
           case BinOp::Mod: return "ifloormod(" + a + ", " + b + ")";
           case BinOp::Min: return "imin(" + a + ", " + b + ")";
           case BinOp::Max: return "imax(" + a + ", " + b + ")";
-          case BinOp::And: return "((i64)((" + a + " != 0) & (" + b + " != 0)))";
-          case BinOp::Or: return "((i64)((" + a + " != 0) | (" + b + " != 0)))";
-          case BinOp::Lt: return "((i64)(" + a + " < " + b + "))";
-          case BinOp::Le: return "((i64)(" + a + " <= " + b + "))";
-          case BinOp::Gt: return "((i64)(" + a + " > " + b + "))";
-          case BinOp::Ge: return "((i64)(" + a + " >= " + b + "))";
-          case BinOp::Eq: return "((i64)(" + a + " == " + b + "))";
-          default: return "((i64)(" + a + " != " + b + "))";
+          case BinOp::And: return "((ix)((" + a + " != 0) & (" + b + " != 0)))";
+          case BinOp::Or: return "((ix)((" + a + " != 0) | (" + b + " != 0)))";
+          case BinOp::Lt: return "((ix)(" + a + " < " + b + "))";
+          case BinOp::Le: return "((ix)(" + a + " <= " + b + "))";
+          case BinOp::Gt: return "((ix)(" + a + " > " + b + "))";
+          case BinOp::Ge: return "((ix)(" + a + " >= " + b + "))";
+          case BinOp::Eq: return "((ix)(" + a + " == " + b + "))";
+          default: return "((ix)(" + a + " != " + b + "))";
         }
       }
       case ExprKind::Unary: {
@@ -158,7 +158,7 @@ struct Gen {
           case UnOp::Exp: isf = true; return "expf(" + as_f(a, fa) + ")";
           case UnOp::Sqrt: isf = true; return "sqrtf(" + as_f(a, fa) + ")";
           case UnOp::CastF32: isf = true; return as_f(a, fa);
-          case UnOp::CastI32: isf = false; return fa ? "((i64)(" + a + "))" : a;
+          case UnOp::CastI32: isf = false; return fa ? "((ix)(" + a + "))" : a;
         }
         throw Unsupported{"unknown unary op"};
       }
@@ -182,7 +182,7 @@ struct Gen {
         for (const auto& i : idx) call += ", " + i;
         call += ")";
         isf = s.tensors[it->second].is_float != 0;
-        return isf ? call : "((i64)" + call + ")";
+        return isf ? call : "((ix)" + call + ")";
       }
       case ExprKind::TableLookup: {
         bool fi;
@@ -196,21 +196,121 @@ struct Gen {
   }
 };
 
+// Interval of every integer-valued subexpression, from the axis extents and the
+// literal constants.  When all of them -- and every offset, extent and integer
+// accumulation -- fit in 32 bits, the generated code computes indices in `int`
+// (half the instructions of 64-bit integer math) with the same results as the
+// interpreter's int64.
+struct Range {
+  bool ok = true;
+  __int128 lo = 0, hi = 0;
+};
+constexpr __int128 kI32Max = 2147483647;
+Range mk(__int128 lo, __int128 hi) {
+  Range r;
+  r.lo = lo;
+  r.hi = hi;
+  r.ok = lo >= -kI32Max && hi <= kI32Max;
+  return r;
+}
+Range bad() {
+  Range r;
+  r.ok = false;
+  return r;
+}
+
+Range int_range(const Expr& e, const RuleSourceSpec& s, const std::map<std::string, int>& var_ix) {
+  switch (e->kind) {
+    case ExprKind::IntImm: return mk(e->ival, e->ival);
+    case ExprKind::FloatImm: return mk(0, 0);  // float: no integer range needed
+    case ExprKind::Var: {
+      auto it = var_ix.find(e->name);
+      if (it == var_ix.end()) return bad();
+      const int v = it->second;
+      const int nsp = static_cast<int>(s.ext.size());
+      const int64_t ext = v < nsp ? s.ext[v] : s.red[v - nsp];
+      return mk(0, ext - 1);
+    }
+    case ExprKind::Load: {
+      for (const auto& a : e->args)
+        if (!int_range(a, s, var_ix).ok) return bad();
+      // an integer tensor's values are data: unbounded; a float load has no integer range
+      for (size_t t = 0; t < s.tensor_names.size(); ++t)
+        if (s.tensor_names[t] == e->name) return s.tensors[t].is_float ? mk(0, 0) : bad();
+      return bad();
+    }
+    case ExprKind::TableLookup: {
+      if (!int_range(e->args[0], s, var_ix).ok) return bad();
+      int64_t lo = 0, hi = 0;
+      for (int64_t v : *e->table) {
+        lo = std::min(lo, v);
+        hi = std::max(hi, v);
+      }
+      return mk(lo, hi);
+    }
+    case ExprKind::Unary: {
+      const Range a = int_range(e->args[0], s, var_ix);
+      if (!a.ok) return bad();
+      switch (e->uop) {
+        case UnOp::Neg: return mk(-a.hi, -a.lo);
+        case UnOp::Relu: return mk(a.lo > 0 ? a.lo : 0, a.hi > 0 ? a.hi : 0);
+        case UnOp::CastI32: return bad();  // float -> int: unbounded
+        default: return mk(0, 0);          // float-valued
+      }
+    }
+    case ExprKind::Select: {
+      const Range c = int_range(e->args[0], s, var_ix), t = int_range(e->args[1], s, var_ix),
+                  f = int_range(e->args[2], s, var_ix);
+      if (!c.ok || !t.ok || !f.ok) return bad();
+      return mk(std::min(t.lo, f.lo), std::max(t.hi, f.hi));
+    }
+    case ExprKind::Binary: {
+      const Range a = int_range(e->args[0], s, var_ix), b = int_range(e->args[1], s, var_ix);
+      if (!a.ok || !b.ok) return bad();
+      switch (e->bop) {
+        case BinOp::Add: return mk(a.lo + b.lo, a.hi + b.hi);
+        case BinOp::Sub: return mk(a.lo - b.hi, a.hi - b.lo);
+        case BinOp::Mul: {
+          const __int128 c[4] = {a.lo * b.lo, a.lo * b.hi, a.hi * b.lo, a.hi * b.hi};
+          return mk(std::min(std::min(c[0], c[1]), std::min(c[2], c[3])),
+                    std::max(std::max(c[0], c[1]), std::max(c[2], c[3])));
+        }
+        case BinOp::Div:
+        case BinOp::Mod: {
+          const __int128 m = std::max(a.hi < 0 ? -a.hi : a.hi, a.lo < 0 ? -a.lo : a.lo);
+          const __int128 d = std::max(b.hi < 0 ? -b.hi : b.hi, b.lo < 0 ? -b.lo : b.lo);
+          return e->bop == BinOp::Div ? mk(-m, m) : mk(-d, d);
+        }
+        case BinOp::Min: return mk(std::min(a.lo, b.lo), std::min(a.hi, b.hi));
+        case BinOp::Max: return mk(std::max(a.lo, b.lo), std::max(a.hi, b.hi));
+        default: return mk(0, 1);  // comparisons, logic
+      }
+    }
+    default: return bad();
+  }
+}
+
+int64_t span_elems(const ev::TensorRef& t) {
+  int64_t s = 1;
+  for (int d = 0; d < t.rank; ++d) s += (t.shape[d] - 1) * (t.stride[d] < 0 ? -t.stride[d] : t.stride[d]);
+  return s;
+}
+
 const char* kPrelude = R"(typedef long long i64;
 struct Ptrs { const void* p[16]; };
 __device__ __forceinline__ float bf2f(unsigned short h) { return __int_as_float(((unsigned)h) << 16); }
 __device__ __forceinline__ float h2f(unsigned short h) { float f; asm("cvt.f32.f16 %0, %1;" : "=f"(f) : "h"(h)); return f; }
 __device__ __forceinline__ unsigned short f2bf(float f) { unsigned short h; asm("cvt.rn.bf16.f32 %0, %1;" : "=h"(h) : "f"(f)); return h; }
 __device__ __forceinline__ unsigned short f2h(float f) { unsigned short h; asm("cvt.rn.f16.f32 %0, %1;" : "=h"(h) : "f"(f)); return h; }
-__device__ __forceinline__ i64 imin(i64 a, i64 b) { return a < b ? a : b; }
-__device__ __forceinline__ i64 imax(i64 a, i64 b) { return a > b ? a : b; }
-__device__ __forceinline__ i64 ifloordiv(i64 a, i64 b) {
+__device__ __forceinline__ ix imin(ix a, ix b) { return a < b ? a : b; }
+__device__ __forceinline__ ix imax(ix a, ix b) { return a > b ? a : b; }
+__device__ __forceinline__ ix ifloordiv(ix a, ix b) {
   if (b == 0) return 0;
-  i64 q = a / b;
+  ix q = a / b;
   if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
   return q;
 }
-__device__ __forceinline__ i64 ifloormod(i64 a, i64 b) { return b == 0 ? 0 : a - ifloordiv(a, b) * b; }
+__device__ __forceinline__ ix ifloormod(ix a, ix b) { return b == 0 ? 0 : a - ifloordiv(a, b) * b; }
 )";
 
 // decomposition of `flat` over `dims` = (variable slot, extent), outermost
@@ -221,7 +321,7 @@ void decompose(std::ostringstream& o, const char* flat, const std::vector<std::p
   int64_t total = 1;
   for (const auto& d : dims) total *= d.second;
   const bool narrow = total < (int64_t(1) << 31);
-  o << ind << "{\n" << ind << "  " << (narrow ? "unsigned rem = (unsigned)" : "i64 rem = ") << flat << ";\n";
+  o << ind << "{\n" << ind << "  " << (narrow ? "unsigned rem = (unsigned)" : "ix rem = ") << flat << ";\n";
   for (int d = static_cast<int>(dims.size()) - 1; d >= 0; --d) {
     if (d == 0) {
       o << ind << "  v" << dims[d].first << " = rem;\n";
@@ -256,7 +356,7 @@ bool emit_rule_source(const RuleSourceSpec& s, std::string& src, std::string& wh
   for (auto e : s.red) red_numel *= e;
   // accumulator type: float when the node or any reduced value is float
   const bool af = nred > 0 ? (s.is_float || vf) : vf;
-  const std::string at = af ? "float" : "i64";
+  const std::string at = af ? "float" : "ix";
   std::string ident, comb_body;
   if (s.combiner == 0) ident = af ? "0.f" : "0LL";
   else if (s.combiner == 1) ident = s.is_float ? "__int_as_float(0xff800000)" : (af ? "(-2147483648.f)" : "(-2147483648LL)");
@@ -265,20 +365,31 @@ bool emit_rule_source(const RuleSourceSpec& s, std::string& src, std::string& wh
   else if (s.combiner == 1) comb_body = af ? "fmaxf(a, b)" : "imax(a, b)";
   else comb_body = af ? "fminf(a, b)" : "imin(a, b)";
 
+  // 32-bit index arithmetic when every integer value provably fits (see Range)
+  bool narrow = numel < (int64_t(1) << 31) && red_numel < (int64_t(1) << 31) && !std::getenv("TMB_RULE_WIDE");
+  const Range vr = int_range(s.expr, s, g.var_ix);
+  narrow = narrow && vr.ok && span_elems(s.out) < (int64_t(1) << 31);
+  for (const auto& t : s.tensors) narrow = narrow && span_elems(t) < (int64_t(1) << 31);
+  for (const auto& t : s.tensors)
+    for (int d = 0; d < t.rank; ++d) narrow = narrow && t.stride[d] < (int64_t(1) << 31) && t.stride[d] > -(int64_t(1) << 31);
+  if (nred > 0 && !af) {  // an integer accumulation: |value| * reduce extent must fit too
+    const __int128 m = std::max(vr.hi < 0 ? -vr.hi : vr.hi, vr.lo < 0 ? -vr.lo : vr.lo);
+    narrow = narrow && m * red_numel <= kI32Max && red_numel <= kI32Max;
+  }
   std::ostringstream o;
-  o << kPrelude;
+  o << (narrow ? "typedef int ix;\n" : "typedef long long ix;\n") << kPrelude;
   o << "__device__ __forceinline__ " << at << " comb(" << at << " a, " << at << " b) { return " << comb_body << "; }\n";
   o << g.helpers.str();
   // output store through the bound strides in the output's storage type
   const ev::TensorRef& out = s.out;
-  o << "__device__ __forceinline__ void put(const Ptrs& P, const i64* v, float x) {\n  const i64 off = 0";
+  o << "__device__ __forceinline__ void put(const Ptrs& P, const ix* v, float x) {\n  const ix off = 0";
   for (int d = 0; d < nsp; ++d) o << " + v[" << d << "] * " << hex_i64(out.stride[d]);
   o << ";\n";
   if (out.store == ev::ST_F32) o << "  ((float*)P.p[15])[off] = x;\n";
   else if (out.store == ev::ST_BF16) o << "  ((unsigned short*)P.p[15])[off] = f2bf(x);\n";
   else o << "  ((unsigned short*)P.p[15])[off] = f2h(x);\n";
   o << "}\n";
-  const std::string vdecl = "i64 v[" + std::to_string(nsp + nred > 0 ? nsp + nred : 1) + "];";
+  const std::string vdecl = "ix v[" + std::to_string(nsp + nred > 0 ? nsp + nred : 1) + "];";
   // the value expression reads v<i>; alias them onto the array
   std::ostringstream alias;
   for (int i = 0; i < nsp + nred; ++i) alias << "#define v" << i << " v[" << i << "]\n";
