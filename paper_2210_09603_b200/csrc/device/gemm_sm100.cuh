@@ -1766,7 +1766,9 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
       // G8: taps adjacent (LBO 128 B along K, SBO 1024 B per 8 rows), 2 taps per K16
       const uint64_t adesc0 = a_noswz ? ptx::smem_desc_noswz(a0, 2048, 128)
                                       : a_g8 ? ptx::smem_desc_noswz(a0, 128, 1024) : ptx::smem_desc_sw128(a0, 16, 1024);
-      const uint64_t bdesc0 = b_mn ? ptx::smem_desc_sw128(b0, mn_lbo, mn_sbo) : ptx::smem_desc_sw128(b0, 16, 1024);
+      const uint64_t bdesc0 = !b_mn ? ptx::smem_desc_sw128(b0, 16, 1024)
+                              : TF32 ? ptx::smem_desc_sw128_base32b(b0, static_cast<uint32_t>(MN_BLOCK_BYTES), 512u)
+                                     : ptx::smem_desc_sw128(b0, mn_lbo, mn_sbo);
       const uint32_t a_kstep = a_noswz ? (2u * 2048u) >> 4
                                        : a_g8 ? (2u * 128u) >> 4 : static_cast<uint32_t>(Cfg::KSTEP * Cfg::kElem) >> 4;
       const uint32_t b_kstep = b_mn ? static_cast<uint32_t>(Cfg::KSTEP * kRowBytes) >> 4

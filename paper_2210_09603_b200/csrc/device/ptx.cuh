@@ -410,6 +410,14 @@ __device__ __forceinline__ uint64_t smem_desc_sw128(uint32_t smem_addr, uint32_t
   return d;
 }
 
+// MN-major 32-bit (kind::tf32) descriptor, layout type 1 (SWIZZLE_128B_BASE32B):
+// 128-byte rows along MN whose 32-byte chunks are permuted by row % 4; LBO = byte
+// stride between 128-byte MN blocks, SBO = between 4-row K groups.
+__device__ __forceinline__ uint64_t smem_desc_sw128_base32b(uint32_t smem_addr, uint32_t lbo_bytes,
+                                                            uint32_t sbo_bytes) {
+  return (smem_desc_sw128(smem_addr, lbo_bytes, sbo_bytes) & ~(7ull << 61)) | (1ull << 61);
+}
+
 // No-swizzle K-major descriptor (layout type 0): core matrices of 8 rows x
 // 16 B; LBO = byte stride between core matrices along K, SBO = along M/N.
 __device__ __forceinline__ uint64_t smem_desc_noswz(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {

@@ -991,6 +991,12 @@ tm::DevMapping tile_mapping(int64_t B, int64_t TM, int64_t TN, int grid, int ras
   return m;
 }
 
+// MN-major fp32 B for kind::tf32 (TMB_TF32_MN=0 restores the gather loader)
+bool tf32_mn_ok() {
+  static const bool on = [] { const char* e = std::getenv("TMB_TF32_MN"); return !(e && e[0] == '0'); }();
+  return on;
+}
+
 // TMA tile views are {K, rows, batch} (K-major) or {rows, K, batch} (MN-major)
 // with strides {row, batch}: the batch stride is encoded as given, so a batch
 // whose stride is below one batch's row span (e.g. heads interleaved inside a
@@ -1582,11 +1588,12 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
                                      (uint64_t)(std::max<int64_t>(f.c2, f.lo * sp.N) * esize(opb->dtype))};
         const uint32_t box[3] = {(uint32_t)BK, (uint32_t)bn_cta, 1u};
         make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * esize(opb->dtype), opb->dtype, 3, dims, strides, box);
-      } else if (!k.tf32 && sp.b.pre.empty() && bn_cta % (128 / esize(want_dt)) == 0 &&
+      } else if ((!k.tf32 || tf32_mn_ok()) && sp.b.pre.empty() && bn_cta % (128 / esize(want_dt)) == 0 &&
                  tma_ok_mnmajor(f, *opb, sp.N, sp.K, sp.batch, want_dt)) {
-        // MN-major B (N contiguous): SWIZZLE_128B rows of MNB = 64 16-bit elements
-        // along N, BK k-rows per block (tcgen05 takes MN-major operands for the
-        // 16-bit kinds only: kind::tf32 B in this layout goes through the gather)
+        // MN-major B (N contiguous): SWIZZLE_128B rows of MNB = 128 B / element
+        // (64 16-bit or 32 fp32 elements) along N, BK k-rows per block.  The SS
+        // form of kind::tf32 takes an MN-major B like the 16-bit kinds (only the
+        // TMEM-A forms require K-major), so row-major fp32 B is TMA-fed too.
         p.b_loader = LD_TMA_MN;
         const int bes = esize(want_dt);
         const uint64_t mnb = 128 / bes;
@@ -1598,13 +1605,15 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
           const uint64_t strides[3] = {(uint64_t)(f.c1 * bes), 128,
                                        (uint64_t)(std::max<int64_t>(f.c2, f.c1 * sp.K) * bes)};
           const uint32_t box[4] = {(uint32_t)mnb, (uint32_t)BK, (uint32_t)(bn_cta / mnb), 1u};
-          make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * bes, opb->dtype, 4, dims, strides, box);
+          make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * bes, opb->dtype, 4, dims, strides, box,
+                        k.tf32 ? kSwizzle128Atom32 : 128);
         } else {
           p.b_mn4d = 0;
           const uint64_t dims[3] = {(uint64_t)sp.N, (uint64_t)sp.K, (uint64_t)sp.batch};
           const uint64_t strides[2] = {(uint64_t)(f.c1 * bes), (uint64_t)(std::max<int64_t>(f.c2, f.c1 * sp.K) * bes)};
           const uint32_t box[3] = {(uint32_t)mnb, (uint32_t)BK, 1u};
-          make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * bes, opb->dtype, 3, dims, strides, box);
+          make_tma_2d3d(k.tma_b, static_cast<const char*>(opb->data) + f.off * bes, opb->dtype, 3, dims, strides, box,
+                        k.tf32 ? kSwizzle128Atom32 : 128);
         }
       } else {
         p.b_loader = LD_GATHER;

@@ -128,7 +128,10 @@ void launch_rule_compiled(void* fn, const RulePtrs& ptrs, unsigned grid, unsigne
 int kernel_mapping_assign(int which, uint32_t worker, int* buf, int cap);
 unsigned long long device_mismatch(const void* a, const void* b, size_t bytes, void* stream);
 float device_max_rel_error(const void* a, const void* b, size_t n, int dtype, void* stream);
-// swizzle: smem swizzle span in bytes (0 = none, 64, 128)
+// swizzle: smem swizzle span in bytes (0 = none, 64, 128), or kSwizzle128Atom32: the
+// 128-byte span with 32-byte atoms (MN-major kind::tf32 operands; UMMA layout type
+// SWIZZLE_128B_BASE32B, 4-row K groups)
+constexpr int kSwizzle128Atom32 = 129;
 void make_tma_2d3d(void* map, const void* ptr, int dtype, int rank, const uint64_t* dims,
                    const uint64_t* strides_bytes, const uint32_t* box, int swizzle = 128);
 void make_tma_im2col(void* map, const void* ptr, int dtype, const uint64_t* dims_cwhn,

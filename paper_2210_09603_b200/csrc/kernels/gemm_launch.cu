@@ -67,8 +67,10 @@ void make_tma_2d3d(void* map, const void* ptr, int dtype, int rank, const uint64
   for (int i = 0; i < rank - 1; ++i) s[i] = strides_bytes[i];
   const CUresult r = enc(reinterpret_cast<CUtensorMap*>(map), tma_dtype(dtype), rank, const_cast<void*>(ptr), d, s, b,
                          e, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                         swizzle == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                        : (swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_NONE),
+                         swizzle == 128   ? CU_TENSOR_MAP_SWIZZLE_128B
+                         : swizzle == kSwizzle128Atom32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                         : swizzle == 64  ? CU_TENSOR_MAP_SWIZZLE_64B
+                                          : CU_TENSOR_MAP_SWIZZLE_NONE,
                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     std::string dims_s, str_s, box_s;

@@ -227,8 +227,8 @@ def test_fp32_cuda_core_tile_variants_exact_int(mnk, bn, bk):
 
 @pytest.mark.parametrize("bn,sk", [(128, 1), (256, 2)])
 def test_matmul_tf32_row_major_b(bn, sk):
-    """kind::tf32 with B [K,N] row-major (MN-major fp32: tcgen05 takes MN-major only for 16-bit
-    kinds, so B is gathered and transposed by the loader warps)."""
+    """kind::tf32 with B [K,N] row-major: MN-major fp32 B TMA-fed in the 32-byte-atom 128-byte
+    swizzle (UMMA layout SWIZZLE_128B_BASE32B, the only MN-major layout kind::tf32 takes)."""
     m, n, k = 512, 384, 256
     rng = port.Rng(13)
     a, b = rounded(rng.tensor((m, k)), "tf32"), rounded(rng.tensor((k, n)), "tf32")
