@@ -50,19 +50,38 @@ struct HbLayout {
 
 namespace detail {
 
+// This CTA's work items [t0, t1).  hb_mc == 1: tiles.  hb_mc == 2: units of the CTA
+// pair (cluster) -- unit u = (spatial pair j, column block f); both CTAs walk the same
+// units, so they consume the same filter stages in the same order (each loads half of
+// every stage and multicasts it to both).
 __device__ __forceinline__ void hb_range(const GemmParams& p, int& t0, int& t1) {
-  const int64_t T = p.hb_total, G = gridDim.x;
-  t0 = static_cast<int>(T * blockIdx.x / G);
-  t1 = static_cast<int>(T * (blockIdx.x + 1) / G);
+  int64_t T = p.hb_total, G = gridDim.x, b = blockIdx.x;
+  if (p.hb_mc == 2) {
+    const int64_t S = p.hb_total / p.hb_ftiles;
+    T = (S + 1) / 2 * p.hb_ftiles;
+    G /= 2;
+    b /= 2;
+  }
+  t0 = static_cast<int>(T * b / G);
+  t1 = static_cast<int>(T * (b + 1) / G);
 }
 
 // tile t -> (image n, first output row oh0, rows in this tile, column tile f)
+// hb_mc == 2: work item t is a pair unit; this CTA (cluster rank r) takes spatial tile
+// 2j + r.  With an odd spatial count the last unit's rank-1 tile is a duplicate of
+// rank 0's (it still walks the shared filter stages) and stores nothing (rows = 0).
 __device__ __forceinline__ void hb_tile(const GemmParams& p, int t, int& n, int& oh0, int& rows, int& f) {
   f = t % p.hb_ftiles;
-  const int s = t / p.hb_ftiles;
+  int s = t / p.hb_ftiles;
+  bool dup = false;
+  if (p.hb_mc == 2) {
+    s = 2 * s + static_cast<int>(blockIdx.x & 1u);
+    dup = s >= p.hb_total / p.hb_ftiles;
+    if (dup) --s;
+  }
   n = s / p.hb_tpi;
   oh0 = (s - n * p.hb_tpi) * p.hb_R;
-  rows = min(p.hb_R, p.conv.ho - oh0);
+  rows = dup ? 0 : min(p.hb_R, p.conv.ho - oh0);
 }
 
 }  // namespace detail
@@ -105,7 +124,7 @@ __global__ void __launch_bounds__(kHbThreads, 1)
     }
     for (int s = 0; s < p.hb_stages; ++s) {
       ptx::mbar_init(&sfull[s], 1);
-      ptx::mbar_init(&sempty[s], 1);
+      ptx::mbar_init(&sempty[s], p.hb_mc);  // both CTAs' MMAs release a shared stage
     }
     ptx::fence_mbar_init();
   }
@@ -119,6 +138,7 @@ __global__ void __launch_bounds__(kHbThreads, 1)
   if (warp == 1) ptx::tmem_alloc<TMEM_COLS>(tmem_slot);
   ptx::tc_fence_before();
   __syncthreads();
+  if (p.hb_mc == 2) ptx::cluster_sync();  // the peer's barriers exist before any multicast lands
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   ptx::griddep_launch_dependents();
@@ -160,7 +180,16 @@ __global__ void __launch_bounds__(kHbThreads, 1)
           ptx::mbar_wait_poll(&sempty[stage], sphase ^ 1u);
           if (lane == 0) {
             ptx::mbar_arrive_expect_tx(&sfull[stage], static_cast<uint32_t>(stage_bytes));
-            ptx::tma_load_4d(ring + stage * stage_bytes, &tmW, &sfull[stage], 0, f * BN, cb, tap0);
+            if (p.hb_mc == 2) {
+              // this CTA's half of the stage (half the taps, or half the filter rows),
+              // multicast into both CTAs of the pair at the same offset
+              const int r = static_cast<int>(blockIdx.x & 1u);
+              ptx::tma_load_4d_mc(ring + stage * stage_bytes + r * (stage_bytes / 2), &tmW, &sfull[stage], 0,
+                                  f * BN + (p.hb_split ? 0 : r * (BN / 2)), cb, tap0 + (p.hb_split ? r * (NB / 2) : 0),
+                                  0x3);
+            } else {
+              ptx::tma_load_4d(ring + stage * stage_bytes, &tmW, &sfull[stage], 0, f * BN, cb, tap0);
+            }
           }
           __syncwarp();
           if (++stage == p.hb_stages) { stage = 0; sphase ^= 1u; }
@@ -170,6 +199,13 @@ __global__ void __launch_bounds__(kHbThreads, 1)
     const int nt = t1 - t0;
     if (nt >= 1) ptx::mbar_wait(&bempty[(nt - 1) & 1], ((nt - 1) >> 1) & 1);
     if (nt >= 2) ptx::mbar_wait(&bempty[(nt - 2) & 1], ((nt - 2) >> 1) & 1);
+    if (p.hb_mc == 2) {
+      // and the peer's releases of the last stages have landed here (no remote
+      // arrival may target this CTA after it exits)
+      const int used = nt * cblocks * ((taps + NB - 1) / NB);
+      for (int u = max(0, used - p.hb_stages); u < used; ++u)
+        ptx::mbar_wait(&sempty[u % p.hb_stages], (u / p.hb_stages) & 1);
+    }
   } else if (warp == 1) {
     // ============================== MMA issuer ==============================
     const uint32_t idesc = ptx::make_idesc(128, BN, p.ab_f16 ? 0u : 1u, false, false);
@@ -178,8 +214,8 @@ __global__ void __launch_bounds__(kHbThreads, 1)
     const uint64_t b0 = ptx::smem_desc_sw128(ptx::smem_u32(ring), 16, 1024);
     const uint32_t band_step = static_cast<uint32_t>(L.band) >> 4;
     const uint32_t g2 = (2u * G16) >> 4;  // K16 step: two channel groups
-    int stage = 0, stage_l = 0;
-    uint32_t sphase = 0, sphase_l = 0;
+    int stage = 0;
+    uint32_t sphase = 0;
     for (int t = t0; t < t1; ++t) {
       const int i = t - t0, bb = i & 1, acc = i & 1;
       ptx::mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
@@ -187,23 +223,24 @@ __global__ void __launch_bounds__(kHbThreads, 1)
       if (lane == 0) detail::rb_trace(p, i, 0, clk0);
       const uint32_t d = tmem_base + acc * BN;
       const uint64_t ab = a0 + bb * band_step;
-      // One elected lane issues the tile: per filter stage, its NB k-blocks' A
-      // offsets (precomputed in smem) are read first, then the stage's 4 NB MMAs go
-      // out as one straight-line burst (looped issue measured ~100+ clk per MMA;
-      // unrolled bursts run near the pacing floor)
-      if (ptx::elect_one()) {
-        constexpr uint32_t bsub = static_cast<uint32_t>(BN * 128) >> 4;  // next tap in a stage
-        int kb = 0;
-        for (int cb = 0; cb < cblocks; ++cb) {
-          ptx::mbar_wait(&bfull[bb * 8 + cb], (i >> 1) & 1);  // this 64-channel chunk of the band
-          for (int tap0 = 0; tap0 < taps; tap0 += NBT) {
-            ptx::mbar_wait(&sfull[stage], sphase);
-            ptx::tc_fence_after();
-            const uint64_t bs = b0 + static_cast<uint64_t>((stage * stage_bytes) >> 4);
-            const int kbn = min(NBT, taps - tap0);
-            uint32_t off[NBT];
+      // The whole warp walks the tile (warp-uniform control flow, descriptors in
+      // uniform registers); one elected lane issues each filter stage's NB k-blocks
+      // as one straight-line burst of 4 NB MMAs and its commit.  (Issuing the whole
+      // tile from a single divergent lane cost ~150 clk per MMA: 610 clk per
+      // k-block on l2.c2 against a ~370 clk warp-uniform floor.)
+      constexpr uint32_t bsub = static_cast<uint32_t>(BN * 128) >> 4;  // next tap in a stage
+      int kb = 0;
+      for (int cb = 0; cb < cblocks; ++cb) {
+        ptx::mbar_wait(&bfull[bb * 8 + cb], (i >> 1) & 1);  // this 64-channel chunk of the band
+        for (int tap0 = 0; tap0 < taps; tap0 += NBT) {
+          ptx::mbar_wait(&sfull[stage], sphase);
+          ptx::tc_fence_after();
+          const uint64_t bs = b0 + static_cast<uint64_t>((stage * stage_bytes) >> 4);
+          const int kbn = min(NBT, taps - tap0);
+          uint32_t off[NBT];
 #pragma unroll
-            for (int s2 = 0; s2 < NBT; ++s2) off[s2] = kbtab[kb + min(s2, kbn - 1)];
+          for (int s2 = 0; s2 < NBT; ++s2) off[s2] = kbtab[kb + min(s2, kbn - 1)];
+          if (ptx::elect_one()) {
 #pragma unroll
             for (int s2 = 0; s2 < NBT; ++s2) {
               if (s2 < kbn) {
@@ -215,19 +252,14 @@ __global__ void __launch_bounds__(kHbThreads, 1)
                                (kb + s2 + q) != 0);
               }
             }
-            ptx::mma_commit(&sempty[stage]);  // stage reusable once these MMAs finish
-            if (++stage == p.hb_stages) { stage = 0; sphase ^= 1u; }
-            kb += kbn;
+            // stage reusable once these MMAs finish (in both CTAs of a pair)
+            if (p.hb_mc == 2) ptx::mma_commit_mc(&sempty[stage], 0x3);
+            else ptx::mma_commit(&sempty[stage]);
           }
+          __syncwarp();
+          if (++stage == p.hb_stages) { stage = 0; sphase ^= 1u; }
+          kb += kbn;
         }
-      }
-      __syncwarp();
-      {  // every lane tracks the ring position the elected lane reached
-        const int nst = cblocks * ((taps + NBT - 1) / NBT);
-        for (int j = 0; j < nst; ++j)
-          if (++stage_l == p.hb_stages) { stage_l = 0; sphase_l ^= 1u; }
-        stage = stage_l;
-        sphase = sphase_l;
       }
       if (ptx::elect_one()) {
         ptx::mma_commit(&tfull[acc]);
@@ -315,6 +347,7 @@ __global__ void __launch_bounds__(kHbThreads, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (p.hb_mc == 2) ptx::cluster_sync();  // both producers' tails done: no arrival in flight
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc<TMEM_COLS>(tmem_base);

@@ -1087,12 +1087,24 @@ bool bind_halo(const SubgraphPlan& sp, const std::map<std::string, tm_tensor>& e
     const uint32_t box[5] = {8u, (uint32_t)P, (uint32_t)rows, 8u, 1u};
     make_tma_2d3d(k.tma_a, x.data, x.dtype, 5, dims, strides, box, 0);
   }
+  // CTA pairs (clusters of 2) share every filter stage: each CTA loads half of it
+  // (half the taps when a stage holds an even number, else half the filter rows) and
+  // multicasts it into both, halving the filter's L2 -> SM traffic.  Opt-in
+  // (TMB_HALO_MC=2): the filter stream does not bound this kernel on the ResNet
+  // layers (measured: equal or slower than one CTA per stage).
+  const int64_t spatial = c.n * ((c.ho + R - 1) / R);
+  const char* mc_env = std::getenv("TMB_HALO_MC");
+  const int mc = mc_env && mc_env[0] == '2' && std::min<int64_t>(sms, spatial * (F / bn)) >= 2 ? 2 : 1;
   {  // filter {64 c, F, C/64 blocks, taps}: a stage is nb taps of one 64-channel block
     const uint64_t taps = c.kh * c.kw;
     const uint64_t dims[4] = {64, (uint64_t)F, (uint64_t)(c.c / 64), taps};
     const uint64_t strides[3] = {(uint64_t)w.stride[0] * 2, 128, (uint64_t)(c.c / 64) * 128};
-    const uint32_t box[4] = {64u, (uint32_t)bn, 1u, (uint32_t)nb};
+    const bool split_taps = nb % 2 == 0;
+    const uint32_t box[4] = {64u, (uint32_t)(mc == 2 && !split_taps ? bn / 2 : bn), 1u,
+                             (uint32_t)(mc == 2 && split_taps ? nb / 2 : nb)};
     make_tma_2d3d(k.tma_b, w.data, w.dtype, 4, dims, strides, box, 128);
+    p.hb_mc = mc;
+    p.hb_split = split_taps ? 1 : 0;
   }
   ConvGeom& g = p.conv;
   g.n = static_cast<int32_t>(c.n); g.c = static_cast<int32_t>(c.c); g.h = static_cast<int32_t>(c.h);
@@ -1118,6 +1130,7 @@ bool bind_halo(const SubgraphPlan& sp, const std::map<std::string, tm_tensor>& e
   k.cg = 1;
   k.smem = halo_smem(band_bytes, nb * bn * 128, stages, bn);
   k.grid = static_cast<int>(std::min<int64_t>(sms, p.hb_total));
+  if (mc == 2) k.grid = static_cast<int>(std::min<int64_t>(sms, 2 * ((spatial + 1) / 2) * p.hb_ftiles)) & ~1;
   if (std::getenv("TMB_TRACE")) {
     void* tr = nullptr;
     const size_t tb = size_t(k.grid) * kTraceTiles * kTraceEvents * 8;

@@ -28,12 +28,19 @@ void launch_hb(const BoundKernel& k, cudaStream_t s) {
   cfg.blockDim = dim3(kHbThreads);
   cfg.dynamicSmemBytes = k.smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   int na = 0;
   static const bool pdl = std::getenv("TMB_NO_PDL") == nullptr;
   if (pdl) {
     attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (k.p.hb_mc == 2) {  // CTA pairs sharing the filter stages (multicast)
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 2;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
     ++na;
   }
   cfg.attrs = attr;

@@ -61,3 +61,16 @@ def test_halo_only_when_scheduled():
     """The halo family is a point of schedule_space('conv2d'): other configs run K3."""
     got, want = _run(1, 64, 20, 64, 3, 1, seed=430, expect_halo=False, cfg=ScheduleConfig())
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("n,c,h,f,k,p", [(1, 64, 56, 64, 3, 1), (3, 128, 28, 128, 3, 1), (2, 256, 14, 256, 3, 1),
+                                         (1, 64, 17, 64, 5, 2), (2, 192, 12, 192, 3, 1)])
+def test_halo_cluster_pair_multicast_exact(monkeypatch, n, c, h, f, k, p):
+    """TMB_HALO_MC=2: CTA pairs (clusters of 2) walk the same filter stages, each
+    TMA-multicasting half of every stage (half the taps when a stage holds an even
+    number, else half the filter rows) into both CTAs, with the MMA commits releasing
+    the stage in both; an odd spatial tile count leaves the last pair's second CTA a
+    duplicate tile that stores nothing."""
+    monkeypatch.setenv("TMB_HALO_MC", "2")
+    got, want = _run(n, c, h, f, k, p, seed=430 + c + h)
+    assert np.array_equal(got, want)
