@@ -214,8 +214,8 @@ __global__ void __launch_bounds__(kHbThreads, 1)
     const uint64_t b0 = ptx::smem_desc_sw128(ptx::smem_u32(ring), 16, 1024);
     const uint32_t band_step = static_cast<uint32_t>(L.band) >> 4;
     const uint32_t g2 = (2u * G16) >> 4;  // K16 step: two channel groups
-    int stage = 0;
-    uint32_t sphase = 0;
+    int stage = 0, stage_l = 0;
+    uint32_t sphase = 0, sphase_l = 0;
     for (int t = t0; t < t1; ++t) {
       const int i = t - t0, bb = i & 1, acc = i & 1;
       ptx::mbar_wait(&tempty[acc], ((i >> 1) & 1) ^ 1);
@@ -223,42 +223,90 @@ __global__ void __launch_bounds__(kHbThreads, 1)
       if (lane == 0) detail::rb_trace(p, i, 0, clk0);
       const uint32_t d = tmem_base + acc * BN;
       const uint64_t ab = a0 + bb * band_step;
-      // The whole warp walks the tile (warp-uniform control flow, descriptors in
-      // uniform registers); one elected lane issues each filter stage's NB k-blocks
-      // as one straight-line burst of 4 NB MMAs and its commit.  (Issuing the whole
-      // tile from a single divergent lane cost ~150 clk per MMA: 610 clk per
-      // k-block on l2.c2 against a ~370 clk warp-uniform floor.)
-      constexpr uint32_t bsub = static_cast<uint32_t>(BN * 128) >> 4;  // next tap in a stage
-      int kb = 0;
-      for (int cb = 0; cb < cblocks; ++cb) {
-        ptx::mbar_wait(&bfull[bb * 8 + cb], (i >> 1) & 1);  // this 64-channel chunk of the band
-        for (int tap0 = 0; tap0 < taps; tap0 += NBT) {
-          ptx::mbar_wait(&sfull[stage], sphase);
-          ptx::tc_fence_after();
-          const uint64_t bs = b0 + static_cast<uint64_t>((stage * stage_bytes) >> 4);
-          const int kbn = min(NBT, taps - tap0);
-          uint32_t off[NBT];
+      if constexpr (NBT >= 4) {
+        // Stages of 4 k-blocks (16 MMAs): the whole warp walks the tile (warp-uniform
+        // control flow, descriptors in uniform registers) and one elected lane issues
+        // each stage's burst and commit.  Smaller stages keep the single-lane walk
+        // below: the per-stage reconvergence costs more than the uniform issue saves
+        // (measured, 1 B200: l1.c2 NB=4 21.3 -> 20.4 us uniform; l2.c2 NB=2 16.2 ->
+        // 17.1 us and l3.c2 NB=1 16.1 -> 18.5 us if made uniform).
+        constexpr uint32_t bsub = static_cast<uint32_t>(BN * 128) >> 4;  // next tap in a stage
+        int kb = 0;
+        for (int cb = 0; cb < cblocks; ++cb) {
+          ptx::mbar_wait(&bfull[bb * 8 + cb], (i >> 1) & 1);  // this 64-channel chunk of the band
+          for (int tap0 = 0; tap0 < taps; tap0 += NBT) {
+            ptx::mbar_wait(&sfull[stage], sphase);
+            ptx::tc_fence_after();
+            const uint64_t bs = b0 + static_cast<uint64_t>((stage * stage_bytes) >> 4);
+            const int kbn = min(NBT, taps - tap0);
+            uint32_t off[NBT];
 #pragma unroll
-          for (int s2 = 0; s2 < NBT; ++s2) off[s2] = kbtab[kb + min(s2, kbn - 1)];
-          if (ptx::elect_one()) {
+            for (int s2 = 0; s2 < NBT; ++s2) off[s2] = kbtab[kb + min(s2, kbn - 1)];
+            if (ptx::elect_one()) {
 #pragma unroll
-            for (int s2 = 0; s2 < NBT; ++s2) {
-              if (s2 < kbn) {
-                const uint64_t ak = ab + off[s2];
-                const uint64_t bk = bs + static_cast<uint64_t>(s2 * bsub);
+              for (int s2 = 0; s2 < NBT; ++s2) {
+                if (s2 < kbn) {
+                  const uint64_t ak = ab + off[s2];
+                  const uint64_t bk = bs + static_cast<uint64_t>(s2 * bsub);
 #pragma unroll
-                for (int q = 0; q < 4; ++q)
-                  ptx::mma_f16(d, ak + static_cast<uint64_t>(q * g2), bk + static_cast<uint64_t>(2 * q), idesc,
-                               (kb + s2 + q) != 0);
+                  for (int q = 0; q < 4; ++q)
+                    ptx::mma_f16(d, ak + static_cast<uint64_t>(q * g2), bk + static_cast<uint64_t>(2 * q), idesc,
+                                 (kb + s2 + q) != 0);
+                }
               }
+              // stage reusable once these MMAs finish (in both CTAs of a pair)
+              if (p.hb_mc == 2) ptx::mma_commit_mc(&sempty[stage], 0x3);
+              else ptx::mma_commit(&sempty[stage]);
             }
-            // stage reusable once these MMAs finish (in both CTAs of a pair)
-            if (p.hb_mc == 2) ptx::mma_commit_mc(&sempty[stage], 0x3);
-            else ptx::mma_commit(&sempty[stage]);
+            __syncwarp();
+            if (++stage == p.hb_stages) { stage = 0; sphase ^= 1u; }
+            kb += kbn;
           }
-          __syncwarp();
-          if (++stage == p.hb_stages) { stage = 0; sphase ^= 1u; }
-          kb += kbn;
+        }
+      } else {
+        // One elected lane issues the tile: per filter stage, its NB k-blocks' A
+        // offsets (precomputed in smem) are read first, then the stage's 4 NB MMAs go
+        // out as one straight-line burst (looped issue measured ~100+ clk per MMA;
+        // unrolled bursts run near the pacing floor)
+        if (ptx::elect_one()) {
+          constexpr uint32_t bsub = static_cast<uint32_t>(BN * 128) >> 4;  // next tap in a stage
+          int kb = 0;
+          for (int cb = 0; cb < cblocks; ++cb) {
+            ptx::mbar_wait(&bfull[bb * 8 + cb], (i >> 1) & 1);  // this 64-channel chunk of the band
+            for (int tap0 = 0; tap0 < taps; tap0 += NBT) {
+              ptx::mbar_wait(&sfull[stage], sphase);
+              ptx::tc_fence_after();
+              const uint64_t bs = b0 + static_cast<uint64_t>((stage * stage_bytes) >> 4);
+              const int kbn = min(NBT, taps - tap0);
+              uint32_t off[NBT];
+#pragma unroll
+              for (int s2 = 0; s2 < NBT; ++s2) off[s2] = kbtab[kb + min(s2, kbn - 1)];
+#pragma unroll
+              for (int s2 = 0; s2 < NBT; ++s2) {
+                if (s2 < kbn) {
+                  const uint64_t ak = ab + off[s2];
+                  const uint64_t bk = bs + static_cast<uint64_t>(s2 * bsub);
+#pragma unroll
+                  for (int q = 0; q < 4; ++q)
+                    ptx::mma_f16(d, ak + static_cast<uint64_t>(q * g2), bk + static_cast<uint64_t>(2 * q), idesc,
+                                 (kb + s2 + q) != 0);
+                }
+              }
+              // stage reusable once these MMAs finish (in both CTAs of a pair)
+              if (p.hb_mc == 2) ptx::mma_commit_mc(&sempty[stage], 0x3);
+              else ptx::mma_commit(&sempty[stage]);
+              if (++stage == p.hb_stages) { stage = 0; sphase ^= 1u; }
+              kb += kbn;
+            }
+          }
+        }
+        __syncwarp();
+        {  // every lane tracks the ring position the elected lane reached
+          const int nst = cblocks * ((taps + NBT - 1) / NBT);
+          for (int j = 0; j < nst; ++j)
+            if (++stage_l == p.hb_stages) { stage_l = 0; sphase_l ^= 1u; }
+          stage = stage_l;
+          sphase = sphase_l;
         }
       }
       if (ptx::elect_one()) {
