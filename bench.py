@@ -326,6 +326,58 @@ def config1_lines(torch, device, peak_tf, sm_mhz, reps=50):
     return out
 
 
+def large_lines(torch, device, peak_tf, reps=10):
+    """north_star target: fused matmul+epilogue and implicit-GEMM conv kernels at
+    >= 70% of the bf16 dense tensor peak on large shapes.  An 8192^3 matmul with the
+    fused bias + ReLU epilogue and two ResNet-50 3x3 conv+BN+ReLU layers at batch 256,
+    each through the product's public Plan API at a few fixed schedules (no tuning);
+    the best schedule is reported, timed as a CUDA graph of `reps` launches (inputs
+    larger than L2 for the GEMM; per-launch traffic mostly L2-resident for the convs)."""
+    from paper_2210_09603_b200 import Graph, Plan, ScheduleConfig, workloads as W
+    g = torch.Generator(device=device)
+    g.manual_seed(13)
+    r = lambda *s, dt=torch.bfloat16: torch.empty(s, device=device).uniform_(-1, 1, generator=g).to(dt)  # noqa: E731
+    out = {}
+
+    def best_of(name, dag, ins, outs, flops, cfgs):
+        best = None
+        for cfg in cfgs:
+            ex = Plan(dag, cfg).bind(ins, outs)
+            gr = Graph([ex] * reps)
+            gr.launch()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            gr.launch()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            if best is None or ms < best[0]:
+                best = (ms, cfg_str(cfg))
+        ms, cs = best
+        tf = flops / (ms / 1e3) / 1e12
+        out[name] = {"ms": round(ms, 4), "tflops": round(tf, 1), "schedule": cs, "frac_of_tensor_peak": round(tf / peak_tf, 4)}
+
+    m = n = k = 8192
+    d = torch.empty((m, n), device=device, dtype=torch.bfloat16)
+    best_of("gemm_8192_bias_relu", W.matmul_bias_relu_dag(m, n, k), [r(m, k), r(k, n), r(n, dt=torch.float32)], [d],
+            2.0 * m * n * k, [ScheduleConfig(block_m=bm, block_n=256) for bm in (256, 128)])
+    del d
+    fmt = torch.channels_last
+    for lname in ("l3.c2", "l4.c2"):
+        L = next(x for x in W.RESNET50 if x.name == lname)
+        B = 256
+        ho = L.out_hw()
+        ins = [r(B, L.c, L.h, L.h).contiguous(memory_format=fmt), r(L.f, L.c, L.k, L.k).contiguous(memory_format=fmt),
+               r(L.f, dt=torch.float32), r(L.f, dt=torch.float32)]
+        o = torch.empty((B, L.f, ho, ho), device=device, dtype=torch.bfloat16).contiguous(memory_format=fmt)
+        best_of(f"conv_{lname}_b{B}_bn_relu", W.conv_bn_relu_dag(L, B), ins, [o], L.flops(B),
+                [ScheduleConfig(block_m=256, block_n=256), ScheduleConfig(block_m=256, block_n=256, split_k=2),
+                 ScheduleConfig(block_m=256, block_n=128), ScheduleConfig(block_m=128, block_n=256),
+                 ScheduleConfig(math="halo")])
+    return out
+
+
 # -------------------------------------------------------------------- main --
 def chain_line(torch, device, rank, world, args, tuner, timed, stream, dist):
     """ResNet-50 v1.5 forward as one chain of the product's
@@ -403,6 +455,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-config1", action="store_true")
     ap.add_argument("--no-chain", action="store_true")
+    ap.add_argument("--no-large", action="store_true", help="skip the large-shape (8192^3, batch-256 conv) lines")
     ap.add_argument("--tune", default="auto", choices=["auto", "force", "off"],
                     help="auto: reuse tuning_cache.json entries, tune the rest on the device")
     ap.add_argument("--tuning-cache", default=os.path.join(ROOT, "tuning_cache.json"))
@@ -570,9 +623,11 @@ def main():
     if not args.no_chain:
         chain = chain_line(torch, device, rank, world, args, tuner, timed, stream, dist)
 
-    c1 = None
+    c1 = large = None
     if rank == 0 and not args.no_config1:
         c1 = config1_lines(torch, device, peaks()[0], clocks.get("sm_mhz"))
+    if rank == 0 and not args.no_large:
+        large = large_lines(torch, device, peaks()[0])
 
     if rank != 0:
         dist.destroy_process_group()
@@ -662,6 +717,7 @@ def main():
         "clocks": clocks,
         "cpu_baseline": cpu,
         "config1": c1,
+        "large_shapes": large,
         "chain": chain,
     }
     print(json.dumps(out))

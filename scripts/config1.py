@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""BASELINE configs[0] lines alone (fp32 CUDA-core, tf32, bf16 forms of 1024^3 + bias + ReLU)."""
+"""BASELINE configs[0] lines alone (fp32 CUDA-core, tf32, bf16 forms of 1024^3 + bias + ReLU);
+--large: bench.py's large-shape lines (8192^3 GEMM, batch-256 ResNet 3x3 convs)."""
 import json
 import os
 import sys
@@ -10,4 +11,8 @@ sys.path.insert(0, ROOT)
 if __name__ == "__main__":
     import torch
     import bench
-    print(json.dumps(bench.config1_lines(torch, torch.device("cuda", 0), bench.peaks()[0], None)))
+    dev = torch.device("cuda", 0)
+    if "--large" in sys.argv:
+        print(json.dumps(bench.large_lines(torch, dev, bench.peaks()[0])))
+    else:
+        print(json.dumps(bench.config1_lines(torch, dev, bench.peaks()[0], None)))
