@@ -627,7 +627,11 @@ def main():
     if rank == 0 and not args.no_config1:
         c1 = config1_lines(torch, device, peaks()[0], clocks.get("sm_mhz"))
     if rank == 0 and not args.no_large:
-        large = large_lines(torch, device, peaks()[0])
+        try:
+            large = large_lines(torch, device, peaks()[0])
+        except Exception as e:  # a reported extra: never fail the headline line over it
+            large = {"error": f"{type(e).__name__}: {e}"[:300]}
+        torch.cuda.empty_cache()
 
     if rank != 0:
         dist.destroy_process_group()
