@@ -622,13 +622,16 @@ __device__ __forceinline__ void add_res4(float (&x)[4], const uint4 (&rq)[4], in
 #define TMB_FT(i) do { } while (0)
 #endif
 
-template <int BN, int CG, int OUT_ROW, int ACT, int RES>
+// F32OUT: fp32 output rows (OUT_ROW == 128: one 32-column group per TMEM load; no
+// residual, no direct stores -- the host admits only those), the same FMA / ReLU.
+template <int BN, int CG, int OUT_ROW, int ACT, int RES, bool F32OUT = false>
 __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t taddr, const float* colbuf,
                                            uint8_t* obuf, int ncols, int32_t col_base, int32_t row0,
                                            int32_t b, int lane, const uint4* res, uint64_t* tempty_bar,
                                            long long* fine = nullptr, __nv_bfloat16* drow = nullptr,
                                            int dcols = 0) {
-  constexpr int GC = OUT_ROW / 2;  // bf16 columns per TMA store group (32 or 64)
+  static_assert(!F32OUT || (OUT_ROW == 128 && RES == 0 && ACT <= 1), "fp32 lean drain: 128-byte rows, no residual");
+  constexpr int GC = OUT_ROW / (F32OUT ? 4 : 2);  // output columns per TMA store group (32 or 64)
   int ft = 0;
   (void)fine;
   (void)ft;
@@ -672,6 +675,29 @@ __device__ __forceinline__ void drain_fast(const CUtensorMap* tmC, uint32_t tadd
       __syncwarp();
     }
     TMB_FT(ft++);
+    if constexpr (F32OUT) {
+      // 32 fp32 columns = the whole 128-byte staged row: 8 swizzled 16-byte chunks
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 sv = *reinterpret_cast<const float4*>(colbuf + c + 4 * q);
+        const float4 tv = *reinterpret_cast<const float4*>(colbuf + BN + c + 4 * q);
+        float x[4] = {fmaf(__uint_as_float(r[4 * q]), sv.x, tv.x), fmaf(__uint_as_float(r[4 * q + 1]), sv.y, tv.y),
+                      fmaf(__uint_as_float(r[4 * q + 2]), sv.z, tv.z), fmaf(__uint_as_float(r[4 * q + 3]), sv.w, tv.w)};
+        if constexpr (ACT == 1) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) x[j] = fmaxf(x[j], 0.f);
+        }
+        *reinterpret_cast<uint4*>(orow + ((q ^ swz) << 4)) =
+            make_uint4(__float_as_uint(x[0]), __float_as_uint(x[1]), __float_as_uint(x[2]), __float_as_uint(x[3]));
+      }
+      ptx::fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        ptx::tma_store_3d(tmC, obuf, col_base + c, row0, b);
+        ptx::bulk_commit();
+      }
+      continue;
+    }
     uint32_t w[16];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -1703,6 +1729,18 @@ __global__ void __launch_bounds__(Roles<GENERIC>::kThreads, 1)
         if (p.trace != nullptr && nvalid <= 4)
           fine = p.trace + (static_cast<int64_t>(blockIdx.x) * kTraceTiles + 48) * kTraceEvents + (nvalid - 1) * 64;
 #endif
+        if constexpr (Cfg::OUT_ROW == 128) {
+          if (p.out_dtype == DT_F32) {  // fp32 rows: identity or ReLU, no residual (host-checked)
+            if (p.canon_act == 1)
+              detail::drain_fast<BN, CG, Cfg::OUT_ROW, 1, 0, true>(&tmC, taddr + cofs, colbuf + cofs, obuf, hcols, cb,
+                                                                   row0, b, lane, nullptr, &tempty[abuf]);
+            else
+              detail::drain_fast<BN, CG, Cfg::OUT_ROW, 0, 0, true>(&tmC, taddr + cofs, colbuf + cofs, obuf, hcols, cb,
+                                                                   row0, b, lane, nullptr, &tempty[abuf]);
+            if (lead) detail::trace(p, i, TR_EPI_DONE, t0);
+            continue;
+          }
+        }
         switch (p.canon_act * 3 + (res == nullptr ? 0 : p.canon_res_pre ? 2 : 1)) {
 #define TMB_DRAIN(A, R)                                                                                          \
   case A * 3 + R:                                                                                                \

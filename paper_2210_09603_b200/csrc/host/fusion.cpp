@@ -1789,6 +1789,17 @@ std::unique_ptr<Exec> bind_plan(const Plan& plan, const tm_tensor* inputs, int n
       int s = k.simt ? 1 : std::max(1, std::min(plan.cfg.split_k, p.num_kb));
       p.kb_per_split = (p.num_kb + s - 1) / s;
       p.split_k = (p.num_kb + p.kb_per_split - 1) / p.kb_per_split;
+      // fp32 output rows through the lean drain too (identity / ReLU epilogue, no
+      // residual, 128-column single-CTA tiles, no split-K): the op-interpreter drain
+      // took ~13k clk per 128x128 fp32 tile against ~2k for the lean one
+      if (!k.simt && p.out_dtype == DT_F32 && p.canon && p.out_tma && !p.out_direct && p.canon_res_op < 0 &&
+          p.canon_act <= 1 && k.cg == 1 && k.bn == 128 && p.split_k == 1 && !std::getenv("TMB_GENERIC") &&
+          !std::getenv("TMB_NO_F32_LEAN")) {
+        const bool a_t = p.a_loader == LD_TMA_K || p.a_loader == LD_IM2COL_TMA || p.a_loader == LD_IM2COL_TMA8;
+        const bool b_t = p.b_loader == LD_TMA_K || p.b_loader == LD_TMA_MN;
+        p.epi_fast = 1;
+        k.generic = (a_t && b_t && !k.tf32) ? 0 : 1;  // the compact instantiation is bf16/fp16-operand only
+      }
       if (p.split_k > 1) {
         const int64_t tiles = int64_t(sp.batch) * p.tiles_m * p.tiles_n * k.cg;
         void* ws = nullptr;
