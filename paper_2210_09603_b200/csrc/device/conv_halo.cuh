@@ -38,9 +38,11 @@ constexpr int kHbMaxKb = 128;    // k-blocks per tile (kh * kw * C / 64)
 struct HbLayout {
   int band, ring, colbuf, kbtab, bars, total;
   __host__ __device__ static int align(int x) { return (x + 1023) & ~1023; }
-  __host__ __device__ HbLayout(int band_bytes, int stage_bytes, int stages, int bn) {
+  // nbands: 2 (the next tile's band loads while this one's MMAs run) or 1 when no CTA
+  // has a second tile (the freed band deepens the filter ring)
+  __host__ __device__ HbLayout(int band_bytes, int stage_bytes, int stages, int bn, int nbands = 2) {
     band = align(band_bytes);
-    ring = 2 * band;
+    ring = nbands * band;
     colbuf = ring + stages * stage_bytes;
     kbtab = colbuf + 4 * bn * 4;  // S / T per epilogue group
     bars = kbtab + kHbMaxKb * 4;
@@ -96,8 +98,8 @@ __global__ void __launch_bounds__(kHbThreads, 1)
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int NB = NBT;  // k-blocks per filter stage (host: p.rb_steps)
   const int stage_bytes = NB * BN * 128;
-  const HbLayout L(p.hb_band, stage_bytes, p.hb_stages, BN);
-  uint8_t* band[2] = {smem, smem + L.band};
+  const HbLayout L(p.hb_band, stage_bytes, p.hb_stages, BN, p.hb_nbands);
+  uint8_t* band[2] = {smem, smem + (p.hb_nbands == 2 ? L.band : 0)};
   uint8_t* ring = smem + L.ring;
   float* colbuf = reinterpret_cast<float*>(smem + L.colbuf);
   uint32_t* kbtab = reinterpret_cast<uint32_t*>(smem + L.kbtab);

@@ -233,6 +233,7 @@ struct GemmParams {
   int32_t hb_stages;   // filter ring depth
   int32_t hb_mc;       // CTAs per cluster sharing (TMA-multicasting) each filter stage: 1 or 2
   int32_t hb_split;    // hb_mc == 2: each CTA loads half a stage -- 1: half the taps, 0: half the rows
+  int32_t hb_nbands;   // band buffers: 2, or 1 when no CTA has a second tile
   int32_t n_ops;
   int32_t has_mat;  // any SIDE_MAT op
   int32_t out_dtype;

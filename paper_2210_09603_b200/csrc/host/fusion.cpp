@@ -1071,11 +1071,19 @@ bool bind_halo(const SubgraphPlan& sp, const std::map<std::string, tm_tensor>& e
   // dead TMEM lanes (r >= R * P) read up to (128 + (kh - 1) P + kw) pixels into the
   // last channel group: slack past the band
   const int band_bytes = G * static_cast<int>(c.c / 8) + (128 + static_cast<int>(c.kh) * P + static_cast<int>(c.kw)) * 16;
+  // eligibility: two bands and a 2-stage ring of single k-blocks fit
+  if (halo_smem(band_bytes, bn * 128, 2, bn, 2) > kMaxSmem) return false;
+  // one band buffer when no CTA gets a second tile (l3.c2 at batch 32: 128 tiles on
+  // 128 CTAs) -- the second band would never be loaded; its space deepens the ring
+  const int64_t tiles_total = c.n * ((c.ho + R - 1) / R) * (F / bn);
+  const char* mc_env0 = std::getenv("TMB_HALO_MC");
+  const bool mc_req = mc_env0 && mc_env0[0] == '2';
+  const int nbands = (!mc_req && tiles_total <= sms && !std::getenv("TMB_HALO_2BANDS")) ? 1 : 2;
   // filter stages of nb k-blocks (32 KB where it fits), the deepest ring that fits
   int nb = 0, stages = 0;
   for (int cand = bn == 64 ? 4 : 2; cand >= 1 && !stages; cand /= 2)
     for (int st = 8; st >= 2 && !stages; --st)
-      if (halo_smem(band_bytes, cand * bn * 128, st, bn) <= kMaxSmem) {
+      if (halo_smem(band_bytes, cand * bn * 128, st, bn, nbands) <= kMaxSmem) {
         stages = st;
         nb = cand;
       }
@@ -1128,7 +1136,8 @@ bool bind_halo(const SubgraphPlan& sp, const std::map<std::string, tm_tensor>& e
   k.rowband = 2;
   k.bn = bn;
   k.cg = 1;
-  k.smem = halo_smem(band_bytes, nb * bn * 128, stages, bn);
+  p.hb_nbands = nbands;
+  k.smem = halo_smem(band_bytes, nb * bn * 128, stages, bn, nbands);
   k.grid = static_cast<int>(std::min<int64_t>(sms, p.hb_total));
   if (mc == 2) k.grid = static_cast<int>(std::min<int64_t>(sms, 2 * ((spatial + 1) / 2) * p.hb_ftiles)) & ~1;
   if (std::getenv("TMB_TRACE")) {

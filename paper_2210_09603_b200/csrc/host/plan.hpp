@@ -116,7 +116,7 @@ void pack_filter(const ConvGeom& g, int kp, void* out, int out_dtype);  // bf16/
 // filter image of the row-band kernel: [kh][steps][bn/8][2][8][8] 16-bit, K order (fw + shift, c < cpad)
 void pack_rowband_filter(const ConvGeom& g, int cpad, int shift, int steps, int bn, void* out, int out_dtype);
 int rowband_smem(int rows, int rowb, int bbytes, int bn);
-int halo_smem(int band_bytes, int stage_bytes, int stages, int bn);
+int halo_smem(int band_bytes, int stage_bytes, int stages, int bn, int nbands = 2);
 // storage dtype of materialised intermediates for these inputs: f32 if any input
 // is f32, fp16 if the 16-bit inputs are all fp16, else bf16
 int intermediate_dtype(const tm_tensor* inputs, int n_in);

@@ -4,8 +4,8 @@
 
 namespace tmb {
 
-int halo_smem(int band_bytes, int stage_bytes, int stages, int bn) {
-  return HbLayout(band_bytes, stage_bytes, stages, bn).total;
+int halo_smem(int band_bytes, int stage_bytes, int stages, int bn, int nbands) {
+  return HbLayout(band_bytes, stage_bytes, stages, bn, nbands).total;
 }
 
 template <int BN, int NB>
